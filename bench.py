@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark: fine-propagator grid-point-updates/s of parareal with splitting propagators.
+
+A step is one parareal iteration of the BASELINE workload (default c3: 4096^2 variable
+kappa, G = FIE, F = DR, N = 64 slices x s = 256 fine steps): the batched fine sweep over
+every local slice, the sequential coarse chain with the fused correction, the NCCL hand-off
+between ranks and the stop-test all-reduce.  value = fine updates (n^d x N x s per step,
+all ranks) / max-over-ranks device time.  One process per GPU (torchrun for N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "fine-propagator grid-point-updates/s"
+UNIT = "updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="prs", choices=["prs", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-launches", action="store_true",
+                    help="under ncu: only a short run, no timing extras")
+    return ap.parse_args()
+
+
+def updates_per_step(p) -> int:
+    return (p.n ** p.dim) * p.N * p.s
+
+
+def workload_config(p, name, n_gpus):
+    sch = {0: "FIE", 1: "DR"}
+    return {"workload": name, "grid": f"{p.n}^{p.dim}", "kappa": "1+0.5sin2pix sin2piy" if p.coef else "1",
+            "split": "dd" if p.split else "dimensional", "pairing": f"{sch[p.G]}-{sch[p.F]}",
+            "N": p.N, "s": p.s, "slices_per_gpu": p.N // n_gpus,
+            "state_MiB": (p.n ** p.dim) * 8 / 2 ** 20,
+            "l2": "inputs larger than L2 (state 128 MiB x 64 slices per pass)" if p.n >= 4096
+            else "working set may be L2-resident"}
+
+
+# --------------------------------------------------------------------- clocks ---
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(name):
+    """dram bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path))
+        except ValueError:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------ CPU oracle ---
+def oracle_sample(p, reps: int = 1):
+    """Time the oracle as it stands on a bounded sample: fine steps of one slice."""
+    import oracle
+    o = oracle.Oracle(p)
+    u = synth.initial_state(p)
+    dt = p.T / (p.N * p.s)
+    t0 = time.perf_counter()
+    for j in range(reps):
+        u = o.step(p.F, dt, float(j + 1) * dt, u)
+    sec = time.perf_counter() - t0
+    upd = reps * p.n ** p.dim
+    sched = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    return upd / sec, sec, {"kind": "oracle", "cores": 1,
+                            "host_cores_available": len(sched) if sched else os.cpu_count(),
+                            "sample": f"{reps} fine {'DR' if p.F else 'FIE'} step(s) of one slice at "
+                                      f"{p.n}^{p.dim} (serial C oracle, -O2, no FMA contraction)"}
+
+
+def oracle_reps_for(p):
+    # about 10 s of serial oracle work per sample
+    per_pt = {2: 0.6e-6 if p.coef else 0.12e-6, 3: 0.15e-6}[p.dim]
+    return max(1, int(10.0 / (per_pt * p.n ** p.dim)))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    p = synth.CONFIGS[args.config]
+    reps = oracle_reps_for(p)
+    for _ in range(args.warmup):
+        oracle_sample(p, 1)
+    times = []
+    rates = []
+    for _ in range(args.steps):
+        r, sec, meta = oracle_sample(p, reps)
+        times.append(sec)
+        rates.append(r)
+    value = float(np.median(rates))
+    meta["value"] = value
+    meta["unit"] = UNIT
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(p, args.config, 1), "cpu_baseline": meta,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm -------
+def run_prs(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_08370_b200 as prs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = synth.CONFIGS[args.config]
+    uid = None
+    if world > 1:
+        obj = [prs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.current_stream()
+    ctx = prs.Context(p, rank=rank, nranks=world, nccl_uid=uid, stream=stream.cuda_stream)
+    u0 = synth.initial_state(p)
+    u0_host = torch.from_numpy(u0).pin_memory()
+    u0_dev = u0_host.cuda()
+    ctx.set_initial(u0_dev)
+    ctx.coarse_sweep()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        ctx.fine_sweep()
+        return ctx.parareal_correct()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.set_profiling(True)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    upds = []
+    for _ in range(args.steps):
+        upds.append(step())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    ms = ev0.elapsed_time(ev1)
+    stats = {k: ctx.kernel_stats(k) for k in (prs.PRS_K_XPASS, prs.PRS_K_LPASS)}
+    ctx.set_profiling(False)
+    clk = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_updates = updates_per_step(p) * args.steps
+    value = total_updates / (ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers (rank-local, then max) ----
+    e2e = None
+    if args.e2e_steps > 0:
+        out_host = torch.empty_like(u0_host).pin_memory()
+        last = ctx.first + ctx.count
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ctx.set_initial(u0_host)          # H2D of the step's input from pinned host memory
+            ctx.coarse_sweep()
+            ctx.fine_sweep()
+            ctx.parareal_correct()            # D2H of the update norm
+            ctx.get_slice(last, out_host)     # D2H of the end state this rank owns
+        barrier()
+        sec = time.perf_counter() - t0
+        st = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        sec = float(st.item())
+        e2e = {"value": updates_per_step(p) * args.e2e_steps / sec, "unit": UNIT,
+               "h2d_bytes_per_step": int(u0.nbytes) * world,
+               "d2h_bytes_per_step": (int(u0.nbytes) + 16) * world,
+               "includes": "set_initial(host) + coarse_sweep + fine_sweep + correct + get_slice(host)"}
+
+    # ---- roofline of the dominant kernel (live CUDA events around each launch) ----
+    dom = max(stats, key=lambda k: stats[k][1])
+    nl, kms, kbytes = stats[dom]
+    peak, peak_src = measured_peaks()
+    achieved = (kbytes / nl) / ((kms / nl) / 1e3) / 1e9 if nl else 0.0
+    names = {prs.PRS_K_XPASS: "xpass_kernel (x-line solve + fused RHS)",
+             prs.PRS_K_LPASS: "lpass_kernel (strided y-line solve + epilogue)"}
+    tr = ncu_traffic(args.config)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": (tr or {}).get(names[dom].split()[0]),
+            "kernel": names[dom], "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": kbytes / nl if nl else None,
+            "avg_launch_ms": kms / nl if nl else None,
+            "share_of_step": kms / ms if ms else None,
+            "other_kernels": {names[k]: {"launches": v[0], "ms": v[1],
+                                         "GBps": (v[2] / v[0]) / ((v[1] / v[0]) / 1e3) / 1e9 if v[0] else None}
+                              for k, v in stats.items()}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sec, meta = oracle_sample(p, oracle_reps_for(p))
+        meta.update({"value": v, "unit": UNIT, "seconds": sec})
+        cpu = meta
+    ctx.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": workload_config(p, args.config, world),
+                "parallelism": f"time-slices x{world}",
+                "updates": upds, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+                "cpu_baseline": cpu, "e2e": e2e}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_prs(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,127 @@
+/*
+ * prs.h -- C ABI of the B200 parareal-with-splitting library (libprs.so).
+ *
+ * Method: arXiv 2502.08370.  The library advances the semi-discrete problem
+ *     U'(t) = (A_1 + ... + A_M) U(t) + F(t),  U(0) = P u_0
+ * on the unit square/cube (interior nodes only, h = 1/(n+1), Dirichlet 0, x-fastest layout)
+ * with the parareal algorithm whose coarse propagator G and fine
+ * propagator F are the splitting integrators FIE or DR
+ * over a dimensional or domain-decomposition split.
+ *
+ * Conventions (all entry points):
+ *   - return PRS_OK (0) or a PRS_E* code; no exception crosses the ABI; prs_last_error()
+ *     returns a per-context message for the last failure.
+ *   - doubles are IEEE fp64; a "state" is n^dim doubles, x fastest (index (k*n + j)*n + i).
+ *   - pointers marked "device" must be device memory of the context's device; they are
+ *     borrowed for the duration of the call; the caller keeps ownership.
+ *   - work is enqueued on the context stream (the one passed to prs_create, or a stream
+ *     the library creates when NULL); calls that return host scalars synchronise it.
+ *   - a context is not thread-safe.
+ */
+#ifndef PRS_H
+#define PRS_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRS_OK 0
+#define PRS_EINVAL 2        /* bad configuration / argument (SPEC.md:472 exit 2)      */
+#define PRS_EDIVERGED 3     /* a non-finite value appeared (exit 3)      */
+#define PRS_EUNSUPPORTED 4  /* valid for the method but not implemented on this path  */
+#define PRS_ECUDA 5         /* CUDA runtime failure                                   */
+#define PRS_ENCCL 6         /* NCCL failure (multi-GPU)                               */
+
+#define PRS_FIE 0
+#define PRS_DR 1
+
+typedef struct prs_ctx prs_ctx;
+
+/* Problem description (mirrors BASELINE.json configs; readings in DESIGN.md §3). */
+typedef struct prs_problem {
+    int dim;          /* 2 or 3                                                          */
+    int n;            /* interior nodes per axis (>= 1)                                  */
+    double c;         /* reaction coefficient, L u = div(kappa grad u) - c u */
+    int coef_kind;    /* 0: kappa = 1;  1: kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y) (2-D) */
+    int split;        /* 0: dimensional, M = dim;  1: domain decomposition, M = 2 (2-D)  */
+    int dd_strips;    /* DD: number of vertical strips 2q (n % dd_strips == 0)           */
+    int dd_overlap;   /* DD: overlap width in cells (even, < n/dd_strips)                */
+    int dd_ramp;      /* DD: 0 linear ramp, 1 cosine ramp                                */
+    int source_kind;  /* 0: F = 0;  1: F = (dim pi^2 + c - 1) e^{-t} prod_d sin(pi x_d)   */
+    double T;         /* final time                                                      */
+    int N;            /* coarse slices N_c, Delta T = T/N                  */
+    int s;            /* fine steps per slice, delta t = Delta T / s                     */
+    int G;            /* coarse scheme PRS_FIE / PRS_DR                                  */
+    int F;            /* fine scheme   PRS_FIE / PRS_DR                                  */
+} prs_problem;
+
+/* Create a context.  Validates the problem before allocating (PRS_EINVAL), allocates the
+ * trajectory, caches and precomputed factors of every stage matrix (I - tau A_j) for
+ * tau in {Delta T, delta t}.  rank/nranks shard the N slices in contiguous
+ * blocks (rank order = time order); nccl_uid is the 128-byte ncclUniqueId from
+ * prs_nccl_unique_id() on rank 0, broadcast by the caller (NULL when nranks == 1).
+ * cuda_stream is a cudaStream_t (NULL: the library creates one). */
+int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_uid,
+               void *cuda_stream, prs_ctx **out);
+
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (call on rank 0 only). */
+int prs_nccl_unique_id(void *uid128);
+
+/* Slices [first, first+count) owned by `rank` out of nranks (host only, no GPU needed). */
+int prs_partition(int N, int nranks, int rank, int *first, int *count);
+
+/* U_0 = P u_0: n^dim doubles, host or device (u0_on_device). */
+int prs_set_initial(prs_ctx *ctx, const double *u0, int u0_on_device);
+
+/* Initial guess U^0_{n+1} = G(U^0_n); also caches G(U^0_n). */
+int prs_coarse_sweep(prs_ctx *ctx);
+
+/* F^s(U^k_n) for every local slice concurrently, then
+ * Delta_n = F^s(U^k_n) - G(U^k_n) in place. */
+int prs_fine_sweep(prs_ctx *ctx);
+
+/* Sequential correction U^{k+1}_{n+1} = G(U^{k+1}_n) + Delta_n; writes the
+ * global normalised update max|U^{k+1} - U^k| / ||U_0||_inf to *update_out (synchronises).
+ * Returns PRS_EDIVERGED if any corrected value is non-finite. */
+int prs_parareal_correct(prs_ctx *ctx, double *update_out);
+
+/* Loop fine_sweep + parareal_correct until update <= tol or k = min(kmax, N) (finite
+ * termination).  hist (kmax doubles, may be NULL) receives the updates. */
+int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist);
+
+/* Copy the current iterate U^k_n (n = 0..N) to host or device memory.  Only the rank that
+ * owns U_n (slice n-1's end state, or n = first for the incoming state) may call it. */
+int prs_get_slice(prs_ctx *ctx, int n, double *out, int out_on_device);
+
+/* One FIE/DR step of size tau from a device state `in` to device `out` (in != out), the
+ * source sampled at t_next = t_{n+1}.  Test hook for per-step parity. */
+int prs_step(prs_ctx *ctx, int scheme, double tau, double t_next, const double *in, double *out);
+
+/* One step of the coarse (which = 0: tau = Delta T, source at (slice0 + b + 1) Delta T) or the
+ * fine (which = 1: tau = delta t, source at ((slice0 + b) s + j + 1) delta t) propagator on B
+ * consecutive device states in -> out (in != out), in the launch configuration of
+ * prs_fine_sweep.  Test hook for full-size batched parity. */
+int prs_step_batch(prs_ctx *ctx, int which, int slice0, int j, const double *in, double *out, int B);
+
+/* Counters.  prs_launches: kernels this context has launched so far.  With profiling on,
+ * every fine-sweep kernel launch is bracketed by CUDA events on the context stream and
+ * prs_kernel_stats(kind) returns, for kind PRS_K_XPASS (contiguous-axis line solve),
+ * PRS_K_LPASS (strided-axis line solve) or PRS_K_DD (DD strip-block stage), the launch
+ * count, the summed device time (ms, synchronises) and the summed ALGORITHMIC bytes
+ * (state read + state write + precomputed factors read). */
+#define PRS_K_XPASS 0
+#define PRS_K_LPASS 1
+#define PRS_K_DD 2
+int prs_set_profiling(prs_ctx *ctx, int on);
+long long prs_launches(const prs_ctx *ctx);
+int prs_kernel_stats(prs_ctx *ctx, int kind, long long *launches, double *ms, double *bytes);
+
+const char *prs_last_error(const prs_ctx *ctx);
+void prs_destroy(prs_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,193 @@
+"""B200-native parareal with splitting propagators (arXiv 2502.08370).
+
+Thin Python binding of the C ABI in ``include/prs.h`` (argument marshalling only).  Every
+step of the method runs in the sm_100a kernels of ``libprs.so``; there is no Python or CPU
+fallback: importing the binding without the built library raises.
+
+    from paper_2502_08370_b200 import Problem, Context
+    ctx = Context(problem, stream=torch.cuda.current_stream().cuda_stream)
+    ctx.set_initial(u0); ctx.coarse_sweep(); k, hist = ctx.iterate(kmax, tol)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._build import SO, build  # noqa: F401
+
+PRS_OK, PRS_EINVAL, PRS_EDIVERGED, PRS_EUNSUPPORTED, PRS_ECUDA, PRS_ENCCL = 0, 2, 3, 4, 5, 6
+PRS_FIE, PRS_DR = 0, 1
+PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
+EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
+           "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
+           "prs_get_slice", "prs_step", "prs_step_batch", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
+           "prs_last_error", "prs_destroy"]
+
+
+class PrsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"prs error {code}: {msg}")
+        self.code = code
+
+
+class prs_problem(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("n", ctypes.c_int), ("c", ctypes.c_double),
+                ("coef_kind", ctypes.c_int), ("split", ctypes.c_int), ("dd_strips", ctypes.c_int),
+                ("dd_overlap", ctypes.c_int), ("dd_ramp", ctypes.c_int),
+                ("source_kind", ctypes.c_int), ("T", ctypes.c_double), ("N", ctypes.c_int),
+                ("s", ctypes.c_int), ("G", ctypes.c_int), ("F", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libprs.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise ImportError(f"{SO} is missing: run paper_2502_08370_b200._build.build() "
+                              "(or __graft_entry__.build()); there is no fallback path")
+        L = ctypes.CDLL(SO)
+        V, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+        PI, PD, PL = ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), \
+            ctypes.POINTER(ctypes.c_longlong)
+        sig = {
+            "prs_create": ([ctypes.POINTER(prs_problem), I, I, V, V, ctypes.POINTER(V)], I),
+            "prs_nccl_unique_id": ([V], I),
+            "prs_partition": ([I, I, I, PI, PI], I),
+            "prs_set_initial": ([V, V, I], I),
+            "prs_coarse_sweep": ([V], I),
+            "prs_fine_sweep": ([V], I),
+            "prs_parareal_correct": ([V, PD], I),
+            "prs_iterate": ([V, I, D, PI, PD], I),
+            "prs_get_slice": ([V, I, V, I], I),
+            "prs_step": ([V, I, D, D, V, V], I),
+            "prs_step_batch": ([V, I, I, I, V, V, I], I),
+            "prs_set_profiling": ([V, I], I),
+            "prs_launches": ([V], ctypes.c_longlong),
+            "prs_kernel_stats": ([V, I, PL, PD, PD], I),
+            "prs_last_error": ([V], ctypes.c_char_p),
+            "prs_destroy": ([V], None),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def to_c_problem(p) -> prs_problem:
+    """Marshal a ``synth.Problem``-like object into the C struct."""
+    return prs_problem(dim=p.dim, n=p.n, c=p.c, coef_kind=p.coef, split=p.split,
+                       dd_strips=p.dd_strips, dd_overlap=p.dd_overlap, dd_ramp=p.dd_ramp,
+                       source_kind=p.source, T=p.T, N=p.N, s=p.s, G=p.G, F=p.F)
+
+
+def partition(N: int, nranks: int, rank: int):
+    first, count = ctypes.c_int(), ctypes.c_int()
+    rc = lib().prs_partition(N, nranks, rank, ctypes.byref(first), ctypes.byref(count))
+    if rc != PRS_OK:
+        raise PrsError(rc, "bad partition arguments")
+    return first.value, count.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().prs_nccl_unique_id(buf)
+    if rc != PRS_OK:
+        raise PrsError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+class Context:
+    """One prs_ctx.  Tensors passed in must be contiguous float64 CUDA tensors (or, for the
+    host-buffer calls, contiguous float64 CPU tensors / numpy arrays)."""
+
+    def __init__(self, prob, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None,
+                 stream: int | None = None):
+        self.L = lib()
+        self.prob = prob
+        self._cp = to_c_problem(prob)
+        h = ctypes.c_void_p()
+        uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid else None
+        rc = self.L.prs_create(ctypes.byref(self._cp), rank, nranks, uid, stream, ctypes.byref(h))
+        if rc != PRS_OK:
+            raise PrsError(rc, "prs_create failed (see stderr)")
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+        self.first, self.count = partition(prob.N, nranks, rank)
+
+    def _check(self, rc):
+        if rc != PRS_OK:
+            raise PrsError(rc, self.L.prs_last_error(self.h).decode())
+        return rc
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.prs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _ptr(x):
+        if hasattr(x, "data_ptr"):
+            return ctypes.c_void_p(x.data_ptr()), bool(x.is_cuda)
+        return ctypes.c_void_p(x.ctypes.data), False
+
+    def set_initial(self, u0):
+        p, dev = self._ptr(u0)
+        self._check(self.L.prs_set_initial(self.h, p, int(dev)))
+
+    def coarse_sweep(self):
+        self._check(self.L.prs_coarse_sweep(self.h))
+
+    def fine_sweep(self):
+        self._check(self.L.prs_fine_sweep(self.h))
+
+    def parareal_correct(self) -> float:
+        upd = ctypes.c_double()
+        self._check(self.L.prs_parareal_correct(self.h, ctypes.byref(upd)))
+        return upd.value
+
+    def iterate(self, kmax: int, tol: float):
+        k = ctypes.c_int()
+        hist = (ctypes.c_double * max(kmax, 1))()
+        rc = self.L.prs_iterate(self.h, kmax, tol, ctypes.byref(k), hist)
+        self._check(rc)
+        return k.value, [hist[i] for i in range(k.value)]
+
+    def get_slice(self, n: int, out):
+        p, dev = self._ptr(out)
+        self._check(self.L.prs_get_slice(self.h, n, p, int(dev)))
+        return out
+
+    def step(self, scheme: int, tau: float, t_next: float, inp, out):
+        pi, _ = self._ptr(inp)
+        po, _ = self._ptr(out)
+        self._check(self.L.prs_step(self.h, scheme, tau, t_next, pi, po))
+        return out
+
+    def step_batch(self, which: int, slice0: int, j: int, inp, out, B: int):
+        pi, _ = self._ptr(inp)
+        po, _ = self._ptr(out)
+        self._check(self.L.prs_step_batch(self.h, which, slice0, j, pi, po, B))
+        return out
+
+    def set_profiling(self, on: bool):
+        self._check(self.L.prs_set_profiling(self.h, int(on)))
+
+    def launches(self) -> int:
+        return int(self.L.prs_launches(self.h))
+
+    def kernel_stats(self, kind: int):
+        n, ms, by = ctypes.c_longlong(), ctypes.c_double(), ctypes.c_double()
+        self._check(self.L.prs_kernel_stats(self.h, kind, ctypes.byref(n), ctypes.byref(ms),
+                                            ctypes.byref(by)))
+        return n.value, ms.value, by.value

@@ -1,0 +1,729 @@
+// prs_api.cu -- C ABI (include/prs.h) and the host-side propagator / parareal driver.
+//
+// Layers: L2 propagators = sequences of line-pass / DD-stage kernels on the
+// context stream; L3 parareal driver = batched fine sweep over all local slices, sequential
+// coarse chain with the fused correction epilogue, stop test, NCCL hand-off of slice end
+// states between ranks (rank order = time order).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/prs.h"
+#include "dd.cuh"
+#include "lines.cuh"
+
+using namespace prs;
+
+namespace {
+
+// ------------------------------------------------------------- NCCL (dlopen) -------
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool load(std::string &err) {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return false;
+        }
+#define SYM(f, name)                                                \
+    f = reinterpret_cast<decltype(f)>(dlsym(h, name));              \
+    if (!f) {                                                       \
+        err = std::string("missing NCCL symbol ") + name;           \
+        return false;                                               \
+    }
+        SYM(GetUniqueId, "ncclGetUniqueId");
+        SYM(CommInitRank, "ncclCommInitRank");
+        SYM(CommDestroy, "ncclCommDestroy");
+        SYM(Send, "ncclSend");
+        SYM(Recv, "ncclRecv");
+        SYM(AllReduce, "ncclAllReduce");
+        SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+        return true;
+    }
+};
+Nccl g_nccl;
+
+}  // namespace
+
+// per-tau pivot data
+struct TauFactors {
+    double tau = -1.0;
+    double *tab = nullptr;               // 3 n (m, id, cc), kappa = 1
+    double *invdx = nullptr, *invdy = nullptr;  // n^2 each, variable kappa
+};
+
+struct prs_ctx {
+    prs_problem p{};
+    int rank = 0, nranks = 1, first = 0, count = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int device = 0;
+    long long vol = 0;
+    size_t sbytes = 0;
+    int M = 2;
+    double h = 0, h2inv = 0, creact = 0, dT = 0, dt = 0;
+    double *traj = nullptr, *fa = nullptr, *fb = nullptr, *gcache = nullptr, *gtmp = nullptr;
+    double *delta = nullptr;  // = fa or fb after a fine sweep
+    double *u0 = nullptr;
+    double *sinpi = nullptr, *s2n = nullptr, *s2f = nullptr;
+    TauFactors fac[3];  // 0 coarse, 1 fine, 2 custom (prs_step)
+    DDData dd;
+    unsigned long long *red = nullptr;  // [0] update bits, [1] flag, [2] scratch
+    unsigned long long *red_host = nullptr;
+    double u0norm = 1.0;
+    bool have_initial = false, have_coarse = false;
+    long long launches = 0;
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, double>> ev_pending;  // (kind, bytes) per recorded pair
+    size_t ev_used = 0;
+    long long k_launch[3] = {0, 0, 0};
+    double k_ms[3] = {0, 0, 0}, k_bytes[3] = {0, 0, 0};
+    ncclComm_t comm = nullptr;
+    std::string err;
+};
+
+#define CK(call)                                                                 \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);       \
+            return PRS_ECUDA;                                                    \
+        }                                                                        \
+    } while (0)
+
+#define NK(call)                                                                 \
+    do {                                                                         \
+        ncclResult_t r_ = (call);                                                \
+        if (r_ != ncclSuccess) {                                                 \
+            ctx->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);     \
+            return PRS_ENCCL;                                                    \
+        }                                                                        \
+    } while (0)
+
+#define TRY(call)                 \
+    do {                          \
+        int rc_ = (call);         \
+        if (rc_ != PRS_OK) return rc_; \
+    } while (0)
+
+static int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+static int last_launch(prs_ctx *ctx) {
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e);
+        return PRS_ECUDA;
+    }
+    return PRS_OK;
+}
+
+// ---- profiling: events around fine-sweep launches ----
+static int prof_begin(prs_ctx *ctx) {
+    if (!ctx->prof) return PRS_OK;
+    while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ctx->ev_pool.push_back(e);
+    }
+    CK(cudaEventRecord(ctx->ev_pool[ctx->ev_used], ctx->stream));
+    return PRS_OK;
+}
+static int prof_end(prs_ctx *ctx, int kind, double bytes) {
+    if (!ctx->prof) return PRS_OK;
+    CK(cudaEventRecord(ctx->ev_pool[ctx->ev_used + 1], ctx->stream));
+    ctx->ev_pending.push_back({kind, bytes});
+    ctx->ev_used += 2;
+    return PRS_OK;
+}
+static int prof_flush(prs_ctx *ctx) {
+    if (ctx->ev_used == 0) return PRS_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (size_t i = 0; i < ctx->ev_pending.size(); ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev_pool[2 * i], ctx->ev_pool[2 * i + 1]));
+        const int k = ctx->ev_pending[i].first;
+        ctx->k_launch[k] += 1;
+        ctx->k_ms[k] += ms;
+        ctx->k_bytes[k] += ctx->ev_pending[i].second;
+    }
+    ctx->ev_pending.clear();
+    ctx->ev_used = 0;
+    return PRS_OK;
+}
+
+// ------------------------------------------------------------------ factors --------
+static int ensure_factors(prs_ctx *ctx, int slot, double tau) {
+    TauFactors &f = ctx->fac[slot];
+    if (f.tau == tau) return PRS_OK;
+    const int n = ctx->p.n;
+    f.tau = tau;
+    if (ctx->p.split == 1) return dd_factors(ctx->dd, slot, tau, ctx->stream, ctx->err);
+    if (ctx->p.coef_kind == 0) {
+        if (!f.tab) CK(cudaMalloc(&f.tab, sizeof(double) * 3 * n));
+        setup_const_tab<<<1, 1, 0, ctx->stream>>>(n, tau, ctx->h2inv, ctx->creact, f.tab, f.tab + n,
+                                                  f.tab + 2 * n);
+        TRY(last_launch(ctx));
+    } else {
+        const size_t bytes = sizeof(double) * (size_t)n * n;
+        if (!f.invdx) CK(cudaMalloc(&f.invdx, bytes));
+        if (!f.invdy) CK(cudaMalloc(&f.invdy, bytes));
+        const int tpb = 128, nb = (n + tpb - 1) / tpb;
+        setup_var_invd<<<nb, tpb, 0, ctx->stream>>>(n, 0, tau, ctx->h2inv, ctx->creact, ctx->s2n,
+                                                    ctx->s2f, f.invdx);
+        TRY(last_launch(ctx));
+        setup_var_invd<<<nb, tpb, 0, ctx->stream>>>(n, 1, tau, ctx->h2inv, ctx->creact, ctx->s2n,
+                                                    ctx->s2f, f.invdy);
+        TRY(last_launch(ctx));
+    }
+    return PRS_OK;
+}
+
+// ----------------------------------------------------------- line-pass launchers ----
+struct EpiArgs {
+    int kind = EPI_STORE;
+    const double *gc = nullptr;   // DELTA
+    double *gcache = nullptr;     // CORRECT/INIT
+    const double *delta = nullptr;
+    double *traj = nullptr;
+};
+
+static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
+                        long long B, const TimeArgs &ta, bool prof) {
+    const int n = ctx->p.n, dim = ctx->p.dim;
+    XArgs a{};
+    a.in = in;
+    a.out = out;
+    a.vol = ctx->vol;
+    a.n = n;
+    a.lines_per_state = (dim == 2) ? n : n * n;
+    a.nlines = B * a.lines_per_state;
+    a.P = next_pow2((n + LCH - 1) / LCH);
+    a.S = cpad_host(n);
+    a.dim = dim;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.creact = ctx->creact;
+    a.src_amp = (double)dim * M_PI * M_PI + ctx->p.c - 1.0;
+    a.sinpi = ctx->sinpi;
+    a.ta = ta;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    a.invd = f.invdx;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    const int threads_target = 256;
+    const int lpb = (a.P >= threads_target) ? 1 : threads_target / a.P;
+    const int threads = lpb * a.P;
+    const int dr = (scheme == PRS_DR) ? 1 : 0;
+    const int coef = ctx->p.coef_kind;
+    const int src = ctx->p.source_kind;
+    size_t shm = sizeof(double) * (size_t)(1 + dr + coef) * lpb * a.S + sizeof(double2) * (threads / 32 + 1);
+    const long long blocks = (a.nlines + lpb - 1) / lpb;
+    void (*kern)(XArgs) = nullptr;
+#define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass_kernel<C, D, S_>;
+    XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
+#undef XK
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    if (prof) TRY(prof_begin(ctx));
+    kern<<<(unsigned)blocks, threads, shm, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    if (prof) {
+        double bytes = (double)B * (double)ctx->vol * (16.0 + (coef ? 8.0 : 0.0));
+        TRY(prof_end(ctx, PRS_K_XPASS, bytes));
+    }
+    return PRS_OK;
+}
+
+// strided pass along axis d (1 = y, 2 = z) over B states in place (in == out allowed)
+static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out,
+                        long long B, const EpiArgs &ep, bool prof) {
+    const int n = ctx->p.n, dim = ctx->p.dim;
+    LArgs a{};
+    a.in = in;
+    a.out = out;
+    a.vol = ctx->vol;
+    a.n = n;
+    if (axis == 1) {
+        a.Sl = n;
+        a.nq = (dim == 2) ? 1 : n;
+        a.Sq = (long long)n * n;
+    } else {
+        a.Sl = (long long)n * n;
+        a.nq = n;
+        a.Sq = n;
+    }
+    a.nwb = (n + PW - 1) / PW;
+    a.npanels = B * a.nq * a.nwb;
+    int CL = 1;
+    while ((n + CL - 1) / CL > 32 * LCH) CL *= 2;
+    if (CL > 8) {
+        ctx->err = "strided line longer than 8 * 512 is not supported";
+        return PRS_EUNSUPPORTED;
+    }
+    a.CL = CL;
+    a.R = (n + CL - 1) / CL;
+    a.CP = next_pow2((a.R + LCH - 1) / LCH);
+    a.S = cpad_host(a.R);
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    a.invd = f.invdy;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    a.e_gc = ep.gc;
+    a.e_gcache = ep.gcache;
+    a.e_delta = ep.delta;
+    a.e_traj = ep.traj;
+    a.e_red = ctx->red;
+    const int coef = ctx->p.coef_kind;
+    const int threads = PW * a.CP;
+    size_t shm = sizeof(double) * (size_t)(1 + coef) * PW * a.S + sizeof(double2) * 2 * PW;
+    void (*kern)(LArgs) = nullptr;
+#define LK(C, E) if (coef == C && ep.kind == E) kern = lpass_kernel<C, E>;
+    LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
+#undef LK
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    if (CL > 1) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(a.npanels * CL));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (prof) TRY(prof_begin(ctx));
+    CK(cudaLaunchKernelEx(&cfg, kern, a));
+    TRY(last_launch(ctx));
+    if (prof) {
+        double per = 16.0 + (coef ? 8.0 : 0.0);
+        if (ep.kind == EPI_DELTA) per += 8.0;
+        TRY(prof_end(ctx, PRS_K_LPASS, (double)B * (double)ctx->vol * per));
+    }
+    return PRS_OK;
+}
+
+// One step of `scheme` on B consecutive states: in -> out (out holds the result, or the
+// epilogue consumes it).  tmp must be distinct from in when scheme is DR.
+static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
+                    long long B, const TimeArgs &ta, const EpiArgs &ep, bool prof) {
+    if (ctx->p.split == 1)
+        return dd_step(ctx->dd, scheme, f.tau, ctx->fac, in, out, B, ta, ep.kind, ep.gc, ep.gcache,
+                       ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err,
+                       ctx->launches);
+    TRY(launch_xpass(ctx, scheme, f, in, out, B, ta, prof));
+    if (ctx->p.dim == 2) return launch_lpass(ctx, 1, f, out, out, B, ep, prof);
+    EpiArgs st;
+    TRY(launch_lpass(ctx, 1, f, out, out, B, st, prof));
+    return launch_lpass(ctx, 2, f, out, out, B, ep, prof);
+}
+
+// hook for dd.cuh profiling
+int prs_internal_prof_begin(prs_ctx *ctx) { return prof_begin(ctx); }
+int prs_internal_prof_end(prs_ctx *ctx, int kind, double bytes) { return prof_end(ctx, kind, bytes); }
+
+static double *state(prs_ctx *ctx, double *base, long long i) { return base + i * ctx->vol; }
+
+// ==================================================================== C ABI =========
+extern "C" {
+
+int prs_partition(int N, int nranks, int rank, int *first, int *count) {
+    if (N < 1 || nranks < 1 || rank < 0 || rank >= nranks || nranks > N) return PRS_EINVAL;
+    const int base = N / nranks, rem = N % nranks;
+    *count = base + (rank < rem ? 1 : 0);
+    *first = rank * base + (rank < rem ? rank : rem);
+    return PRS_OK;
+}
+
+int prs_nccl_unique_id(void *uid128) {
+    std::string err;
+    if (!g_nccl.load(err)) return PRS_ENCCL;
+    ncclUniqueId id;
+    if (g_nccl.GetUniqueId(&id) != ncclSuccess) return PRS_ENCCL;
+    memcpy(uid128, &id, sizeof(id));
+    return PRS_OK;
+}
+
+static int validate(const prs_problem *p, std::string &err) {
+    if (!p) { err = "null problem"; return PRS_EINVAL; }
+    if (p->dim != 2 && p->dim != 3) { err = "dim must be 2 or 3"; return PRS_EINVAL; }
+    if (p->n < 1) { err = "n must be >= 1"; return PRS_EINVAL; }
+    if (!(p->c >= 0.0) || !(p->T > 0.0)) { err = "need c >= 0 and T > 0"; return PRS_EINVAL; }
+    if (p->N < 1 || p->s < 1) { err = "need N >= 1 and s >= 1"; return PRS_EINVAL; }
+    if ((p->G != PRS_FIE && p->G != PRS_DR) || (p->F != PRS_FIE && p->F != PRS_DR)) {
+        err = "schemes must be PRS_FIE or PRS_DR";
+        return PRS_EINVAL;
+    }
+    if (p->coef_kind != 0 && p->coef_kind != 1) { err = "coef_kind must be 0 or 1"; return PRS_EINVAL; }
+    if (p->source_kind != 0 && p->source_kind != 1) { err = "source_kind must be 0 or 1"; return PRS_EINVAL; }
+    if (p->split != 0 && p->split != 1) { err = "split must be 0 or 1"; return PRS_EINVAL; }
+    if (p->split == 1) {
+        if (p->dim != 2) { err = "DD splitting is 2-D"; return PRS_EUNSUPPORTED; }
+        if (p->dd_strips < 1 || p->n % p->dd_strips != 0) {
+            err = "n must be a multiple of dd_strips";
+            return PRS_EINVAL;
+        }
+        if (p->dd_overlap < 0 || p->dd_overlap % 2 != 0 || p->dd_overlap >= p->n / p->dd_strips) {
+            err = "dd_overlap must be even and smaller than the strip width";
+            return PRS_EINVAL;
+        }
+        if (p->dd_ramp != 0 && p->dd_ramp != 1) { err = "dd_ramp must be 0 or 1"; return PRS_EINVAL; }
+    }
+    if (p->dim == 3 && p->coef_kind != 0) { err = "variable kappa is 2-D only"; return PRS_EUNSUPPORTED; }
+    if (p->dim == 3 && (p->G == PRS_DR || p->F == PRS_DR)) {
+        err = "3-D Douglas-Rachford (M = 3) is not implemented on the GPU path";
+        return PRS_EUNSUPPORTED;
+    }
+    if (p->split == 0 && p->n > 8 * 32 * LCH) { err = "n too large for the line kernels"; return PRS_EUNSUPPORTED; }
+    return PRS_OK;
+}
+
+void prs_destroy(prs_ctx *ctx);
+
+int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_uid, void *cuda_stream,
+               prs_ctx **out) {
+    if (!out) return PRS_EINVAL;
+    *out = nullptr;
+    std::string verr;
+    int rc = validate(prob, verr);
+    if (rc != PRS_OK) {
+        fprintf(stderr, "prs_create: %s\n", verr.c_str());
+        return rc;
+    }
+    int first = 0, count = 0;
+    if (prs_partition(prob->N, nranks, rank, &first, &count) != PRS_OK) return PRS_EINVAL;
+    if (nranks > 1 && !nccl_uid) return PRS_EINVAL;
+    prs_ctx *ctx = new prs_ctx();
+    ctx->p = *prob;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->first = first;
+    ctx->count = count;
+    const int n = prob->n;
+    ctx->vol = (prob->dim == 2) ? (long long)n * n : (long long)n * n * n;
+    ctx->sbytes = sizeof(double) * (size_t)ctx->vol;
+    ctx->M = (prob->split == 1) ? 2 : prob->dim;
+    ctx->h = 1.0 / (double)(n + 1);
+    ctx->h2inv = (double)(n + 1) * (double)(n + 1);
+    ctx->creact = prob->c / (double)ctx->M;
+    ctx->dT = prob->T / (double)prob->N;
+    ctx->dt = prob->T / ((double)prob->N * (double)prob->s);
+    *out = ctx;
+#define CKC(call)                                                                \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);       \
+            fprintf(stderr, "prs_create: %s\n", ctx->err.c_str());               \
+            prs_destroy(ctx);                                                    \
+            *out = nullptr;                                                      \
+            return PRS_ECUDA;                                                    \
+        }                                                                        \
+    } while (0)
+    CKC(cudaGetDevice(&ctx->device));
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+        CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    const size_t sb = ctx->sbytes;
+    CKC(cudaMalloc(&ctx->traj, sb * (count + 1)));
+    CKC(cudaMalloc(&ctx->fa, sb * count));
+    CKC(cudaMalloc(&ctx->fb, sb * count));
+    CKC(cudaMalloc(&ctx->gcache, sb * count));
+    CKC(cudaMalloc(&ctx->gtmp, sb));
+    CKC(cudaMalloc(&ctx->u0, sb));
+    CKC(cudaMalloc(&ctx->sinpi, sizeof(double) * n));
+    CKC(cudaMalloc(&ctx->s2n, sizeof(double) * n));
+    CKC(cudaMalloc(&ctx->s2f, sizeof(double) * (n + 1)));
+    CKC(cudaMalloc(&ctx->red, sizeof(unsigned long long) * 4));
+    CKC(cudaMallocHost(&ctx->red_host, sizeof(unsigned long long) * 4));
+    setup_sines<<<(n + 1 + 255) / 256, 256, 0, ctx->stream>>>(n, ctx->h, ctx->sinpi, ctx->s2n, ctx->s2f);
+    ctx->launches++;
+    CKC(cudaGetLastError());
+    if (prob->split == 1) {
+        int drc = dd_init(ctx->dd, *prob, ctx->h, ctx->h2inv, ctx->stream, ctx->err);
+        if (drc != PRS_OK) {
+            fprintf(stderr, "prs_create: %s\n", ctx->err.c_str());
+            prs_destroy(ctx);
+            *out = nullptr;
+            return drc;
+        }
+        ctx->dd.sinpi = ctx->sinpi;
+    }
+    int frc = ensure_factors(ctx, 0, ctx->dT);
+    if (frc == PRS_OK) frc = ensure_factors(ctx, 1, ctx->dt);
+    if (frc != PRS_OK) {
+        fprintf(stderr, "prs_create: %s\n", ctx->err.c_str());
+        prs_destroy(ctx);
+        *out = nullptr;
+        return frc;
+    }
+    if (nranks > 1) {
+        std::string e;
+        if (!g_nccl.load(e)) {
+            fprintf(stderr, "prs_create: %s\n", e.c_str());
+            prs_destroy(ctx);
+            *out = nullptr;
+            return PRS_ENCCL;
+        }
+        ncclUniqueId id;
+        memcpy(&id, nccl_uid, sizeof(id));
+        if (g_nccl.CommInitRank(&ctx->comm, nranks, id, rank) != ncclSuccess) {
+            fprintf(stderr, "prs_create: ncclCommInitRank failed\n");
+            ctx->comm = nullptr;
+            prs_destroy(ctx);
+            *out = nullptr;
+            return PRS_ENCCL;
+        }
+    }
+    CKC(cudaStreamSynchronize(ctx->stream));
+#undef CKC
+    return PRS_OK;
+}
+
+void prs_destroy(prs_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+    double *bufs[] = {ctx->traj, ctx->fa, ctx->fb, ctx->gcache, ctx->gtmp, ctx->u0,
+                      ctx->sinpi, ctx->s2n, ctx->s2f};
+    for (double *b : bufs)
+        if (b) cudaFree(b);
+    for (auto &f : ctx->fac) {
+        if (f.tab) cudaFree(f.tab);
+        if (f.invdx) cudaFree(f.invdx);
+        if (f.invdy) cudaFree(f.invdy);
+    }
+    dd_free(ctx->dd);
+    if (ctx->red) cudaFree(ctx->red);
+    if (ctx->red_host) cudaFreeHost(ctx->red_host);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *prs_last_error(const prs_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int prs_set_initial(prs_ctx *ctx, const double *u0, int u0_on_device) {
+    if (!ctx || !u0) return PRS_EINVAL;
+    CK(cudaMemcpyAsync(ctx->u0, u0, ctx->sbytes, u0_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream));
+    if (ctx->rank == 0) CK(cudaMemcpyAsync(ctx->traj, ctx->u0, ctx->sbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->red + 2, 0, sizeof(unsigned long long), ctx->stream));
+    absmax_kernel<<<148 * 4, 256, 0, ctx->stream>>>(ctx->u0, ctx->vol, ctx->red + 2);
+    TRY(last_launch(ctx));
+    CK(cudaMemcpyAsync(ctx->red_host + 2, ctx->red + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double nrm;
+    memcpy(&nrm, ctx->red_host + 2, sizeof(double));
+    ctx->u0norm = (nrm > 0.0) ? nrm : 1.0;
+    ctx->have_initial = true;
+    ctx->have_coarse = false;
+    return PRS_OK;
+}
+
+static TimeArgs coarse_time(prs_ctx *ctx, int slice) {
+    TimeArgs ta;
+    ta.slice0 = slice;
+    ta.tmul = 1;
+    ta.toff = 1;
+    ta.tstep = ctx->dT;
+    return ta;
+}
+
+int prs_coarse_sweep(prs_ctx *ctx) {
+    if (!ctx) return PRS_EINVAL;
+    if (!ctx->have_initial) { ctx->err = "prs_set_initial first"; return PRS_EINVAL; }
+    TRY(ensure_factors(ctx, 0, ctx->dT));
+    if (ctx->nranks > 1 && ctx->rank > 0)
+        NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    for (int i = 0; i < ctx->count; ++i) {
+        EpiArgs ep;
+        ep.kind = EPI_INIT;
+        ep.gcache = state(ctx, ctx->gcache, i);
+        ep.traj = state(ctx, ctx->traj, i + 1);
+        TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
+                     coarse_time(ctx, ctx->first + i), ep, false));
+    }
+    if (ctx->nranks > 1 && ctx->rank < ctx->nranks - 1)
+        NK(g_nccl.Send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ncclDouble, ctx->rank + 1, ctx->comm,
+                       ctx->stream));
+    ctx->have_coarse = true;
+    return PRS_OK;
+}
+
+int prs_fine_sweep(prs_ctx *ctx) {
+    if (!ctx) return PRS_EINVAL;
+    if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
+    TRY(ensure_factors(ctx, 1, ctx->dt));
+    const int s = ctx->p.s;
+    const double *src = ctx->traj;
+    double *bufs[2] = {ctx->fa, ctx->fb};
+    for (int j = 0; j < s; ++j) {
+        double *dst = bufs[j & 1];
+        TimeArgs ta;
+        ta.slice0 = ctx->first;
+        ta.tmul = s;
+        ta.toff = j + 1;
+        ta.tstep = ctx->dt;
+        EpiArgs ep;
+        if (j == s - 1) {
+            ep.kind = EPI_DELTA;
+            ep.gc = ctx->gcache;
+        }
+        TRY(run_step(ctx, ctx->p.F, ctx->fac[1], src, dst, ctx->count, ta, ep, ctx->prof));
+        src = dst;
+        ctx->delta = dst;
+    }
+    if (ctx->prof) TRY(prof_flush(ctx));
+    return PRS_OK;
+}
+
+int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
+    if (!ctx) return PRS_EINVAL;
+    if (!ctx->delta) { ctx->err = "prs_fine_sweep first"; return PRS_EINVAL; }
+    CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
+    if (ctx->nranks > 1 && ctx->rank > 0)
+        NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    for (int i = 0; i < ctx->count; ++i) {
+        EpiArgs ep;
+        ep.kind = EPI_CORRECT;
+        ep.gcache = state(ctx, ctx->gcache, i);
+        ep.delta = state(ctx, ctx->delta, i);
+        ep.traj = state(ctx, ctx->traj, i + 1);
+        TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
+                     coarse_time(ctx, ctx->first + i), ep, false));
+    }
+    if (ctx->nranks > 1) {
+        if (ctx->rank < ctx->nranks - 1)
+            NK(g_nccl.Send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ncclDouble, ctx->rank + 1,
+                           ctx->comm, ctx->stream));
+        NK(g_nccl.AllReduce(ctx->red, ctx->red, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    }
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double upd;
+    memcpy(&upd, ctx->red_host, sizeof(double));
+    if (update_out) *update_out = upd / ctx->u0norm;
+    ctx->delta = nullptr;
+    if (ctx->red_host[1]) {
+        ctx->err = "non-finite value in the parareal iterate";
+        return PRS_EDIVERGED;
+    }
+    return PRS_OK;
+}
+
+int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
+    if (!ctx || kmax < 0) return PRS_EINVAL;
+    const int K = kmax < ctx->p.N ? kmax : ctx->p.N;
+    int k = 0;
+    int rc = PRS_OK;
+    for (; k < K;) {
+        TRY(prs_fine_sweep(ctx));
+        double upd = 0.0;
+        rc = prs_parareal_correct(ctx, &upd);
+        if (hist) hist[k] = upd;
+        ++k;
+        if (rc != PRS_OK) break;
+        if (upd <= tol) break;
+    }
+    if (k_out) *k_out = k;
+    return rc;
+}
+
+int prs_get_slice(prs_ctx *ctx, int n, double *out, int out_on_device) {
+    if (!ctx || !out) return PRS_EINVAL;
+    const int i = n - ctx->first;
+    if (i < 0 || i > ctx->count) { ctx->err = "slice not owned by this rank"; return PRS_EINVAL; }
+    CK(cudaMemcpyAsync(out, state(ctx, ctx->traj, i), ctx->sbytes,
+                       out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PRS_OK;
+}
+
+int prs_step(prs_ctx *ctx, int scheme, double tau, double t_next, const double *in, double *out) {
+    if (!ctx || !in || !out || in == out || !(tau > 0.0)) return PRS_EINVAL;
+    if (scheme != PRS_FIE && scheme != PRS_DR) return PRS_EINVAL;
+    if (ctx->p.dim == 3 && scheme == PRS_DR) return PRS_EUNSUPPORTED;
+    int slot = 2;
+    if (tau == ctx->fac[0].tau) slot = 0;
+    else if (tau == ctx->fac[1].tau) slot = 1;
+    TRY(ensure_factors(ctx, slot, tau));
+    TimeArgs ta;
+    ta.slice0 = 0;
+    ta.tmul = 0;
+    ta.toff = 1;
+    ta.tstep = t_next;
+    EpiArgs ep;
+    TRY(run_step(ctx, scheme, ctx->fac[slot], in, out, 1, ta, ep, false));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PRS_OK;
+}
+
+int prs_step_batch(prs_ctx *ctx, int which, int slice0, int j, const double *in, double *out, int B) {
+    if (!ctx || !in || !out || in == out || B < 1 || (which != 0 && which != 1)) return PRS_EINVAL;
+    TRY(ensure_factors(ctx, which, which == 0 ? ctx->dT : ctx->dt));
+    TimeArgs ta;
+    ta.slice0 = slice0;
+    ta.tmul = (which == 0) ? 1 : ctx->p.s;
+    ta.toff = (which == 0) ? 1 : j + 1;
+    ta.tstep = (which == 0) ? ctx->dT : ctx->dt;
+    EpiArgs ep;
+    TRY(run_step(ctx, which == 0 ? ctx->p.G : ctx->p.F, ctx->fac[which], in, out, B, ta, ep, false));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PRS_OK;
+}
+
+int prs_set_profiling(prs_ctx *ctx, int on) {
+    if (!ctx) return PRS_EINVAL;
+    ctx->prof = on != 0;
+    for (int k = 0; k < 3; ++k) {
+        ctx->k_launch[k] = 0;
+        ctx->k_ms[k] = 0;
+        ctx->k_bytes[k] = 0;
+    }
+    return PRS_OK;
+}
+
+long long prs_launches(const prs_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+int prs_kernel_stats(prs_ctx *ctx, int kind, long long *launches, double *ms, double *bytes) {
+    if (!ctx || kind < 0 || kind > 2) return PRS_EINVAL;
+    TRY(prof_flush(ctx));
+    if (launches) *launches = ctx->k_launch[kind];
+    if (ms) *ms = ctx->k_ms[kind];
+    if (bytes) *bytes = ctx->k_bytes[kind];
+    return PRS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Bar (BASELINE north_star, R13): per iteration k,
+    e_k = max_{n,i} |gpu - cpu| / max(||U_0||_inf, max_n ||cpu^k_n||_inf) <= 1e-11.
+Single steps use the same normalisation with the step's input and output.
+Inputs are seeded synthetic fields from ``synth``; no oracle input or expected value comes
+from the CUDA path.
+"""
+from __future__ import annotations
+
+import math
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import DR, FIE, Problem
+from tests import modal
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08370_b200 as prs
+    prs.lib()  # the native library must load: no fallback
+    yield
+
+
+def prs_mod():
+    import paper_2502_08370_b200 as prs
+    return prs
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def nerr(gpu, cpu, *scales):
+    s = max([float(np.max(np.abs(x))) for x in scales] + [1e-300])
+    return float(np.max(np.abs(np.asarray(gpu) - np.asarray(cpu)))) / s
+
+
+def rand_field(p, seed):
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal((p.n,) * p.dim)
+
+
+# ------------------------------------------------------------ single steps
+STEP_CASES = []
+for n in (1, 2, 5, 16, 17, 31, 64, 100, 256, 257, 513, 1100):
+    for coef in (0, 1):
+        for src in (0, 1):
+            STEP_CASES.append(Problem(dim=2, n=n, c=1.0, coef=coef, source=src, N=4, s=3))
+for n in (1, 5, 17, 40):
+    STEP_CASES.append(Problem(dim=3, n=n, c=1.0, source=1, N=4, s=3))
+
+
+@pytest.mark.parametrize("p", STEP_CASES, ids=lambda p: f"{p.dim}d_n{p.n}_k{p.coef}_f{p.source}")
+def test_single_step_parity(p):
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    o = oracle.Oracle(p)
+    u = rand_field(p, 11 + p.n)
+    du = dev(u)
+    out = torch.empty_like(du)
+    schemes = (FIE, DR) if p.dim == 2 else (FIE,)
+    for sch in schemes:
+        for tau, tn in ((1e-4, 0.3), (0.37, 0.74)):
+            ctx.step(sch, tau, tn, du, out)
+            want = o.step(sch, tau, tn, u)
+            e = nerr(host(out), want, want, u)
+            assert e <= TOL, (sch, tau, e)
+    ctx.close()
+
+
+def test_dr_unsupported_in_3d_is_loud():
+    prs = prs_mod()
+    p = Problem(dim=3, n=8, N=2, s=2)
+    ctx = prs.Context(p)
+    x = dev(np.zeros((8, 8, 8)))
+    with pytest.raises(prs.PrsError) as ei:
+        ctx.step(DR, 0.1, 0.1, x, torch.empty_like(x))
+    assert ei.value.code == prs.PRS_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("p", [Problem(dim=2, n=77, coef=1, N=6, s=5, G=FIE, F=DR, source=0),
+                               Problem(dim=2, n=64, coef=0, N=6, s=5, G=DR, F=FIE, source=1),
+                               Problem(dim=3, n=21, N=6, s=5, source=1)],
+                         ids=lambda p: p.label())
+def test_batched_step_parity(p):
+    """prs_step_batch runs the exact launch configuration of the fine sweep over B states."""
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    o = oracle.Oracle(p)
+    B = 5
+    us = np.stack([rand_field(p, 100 + b) for b in range(B)])
+    du = dev(us)
+    out = torch.empty_like(du)
+    dt = p.T / (p.N * p.s)
+    dT = p.T / p.N
+    for which, j in ((1, 0), (1, 3), (0, 0)):
+        ctx.step_batch(which, 1, j, du, out, B)
+        got = host(out)
+        for b in range(B):
+            if which == 1:
+                want = o.step(p.F, dt, float((1 + b) * p.s + j + 1) * dt, us[b])
+            else:
+                want = o.step(p.G, dT, float(1 + b + 1) * dT, us[b])
+            assert nerr(got[b], want, want, us[b]) <= TOL
+    ctx.close()
+
+
+# ------------------------------------------------------- whole parareal runs
+def gpu_parareal(p, u0, K):
+    """Run coarse sweep + K iterations; return per-k trajectories and updates."""
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    ctx.set_initial(dev(u0))
+    ctx.coarse_sweep()
+    buf = torch.empty((p.n,) * p.dim, dtype=torch.float64, device="cuda")
+
+    def traj():
+        return np.stack([host(ctx.get_slice(n, buf)).copy() for n in range(p.N + 1)])
+
+    trajs, upds = [traj()], []
+    for _ in range(K):
+        ctx.fine_sweep()
+        upds.append(ctx.parareal_correct())
+        trajs.append(traj())
+    ctx.close()
+    return trajs, upds
+
+
+PARAREAL_CASES = [
+    synth.CONFIGS["c0"],
+    Problem(dim=2, n=48, c=1.0, N=8, s=8, G=DR, F=DR, init="modes", seed=0),        # c1 recipe
+    Problem(dim=2, n=80, c=1.0, coef=1, N=6, s=8, G=FIE, F=DR, init="modes", seed=1),  # c3 recipe
+    Problem(dim=2, n=80, c=1.0, coef=1, N=6, s=8, G=DR, F=DR, init="modes", seed=2),
+    Problem(dim=3, n=20, c=1.0, source=1, N=5, s=4, G=FIE, F=FIE),                  # c2 recipe
+    Problem(dim=2, n=37, c=1.0, source=1, N=5, s=3, G=DR, F=FIE),
+    Problem(dim=2, n=37, c=1.0, source=1, N=5, s=3, G=FIE, F=DR),
+]
+
+
+@pytest.mark.parametrize("p", PARAREAL_CASES, ids=lambda p: p.label())
+def test_parareal_iterates_match_oracle_every_iteration(p):
+    """A13: every iterate U^k_n, k = 0..N, and the update norms."""
+    u0 = synth.initial_state(p)
+    o = oracle.Oracle(p)
+    K = p.N
+    ctrajs, cupds = o.parareal(u0, K, fixed=True)
+    gtrajs, gupds = gpu_parareal(p, u0, K)
+    for k in range(K + 1):
+        scale = max(float(np.max(np.abs(u0))), float(np.max(np.abs(ctrajs[k]))))
+        e = float(np.max(np.abs(gtrajs[k] - ctrajs[k]))) / scale
+        assert e <= TOL, (k, e)
+    for k in range(K):
+        scale = max(1.0, max(float(np.max(np.abs(t))) for t in ctrajs[: k + 2]) / np.max(np.abs(u0)))
+        assert abs(gupds[k] - cupds[k]) <= TOL * scale, (k, gupds[k], cupds[k])
+    # finite termination on the GPU: U^N = sequential fine solution
+    fine = o.fine_solution(u0)
+    scale = max(float(np.max(np.abs(t))) for t in ctrajs)
+    assert float(np.max(np.abs(gtrajs[K] - fine))) / scale <= TOL
+
+
+def test_iterate_stop_rule_and_determinism():
+    """prs_iterate stops at update <= tol or k = N; two runs are bitwise identical (P12)."""
+    prs = prs_mod()
+    p = Problem(dim=2, n=40, c=1.0, coef=1, N=8, s=6, G=FIE, F=DR, init="modes", seed=3)
+    u0 = synth.initial_state(p)
+    outs = []
+    for _ in range(2):
+        ctx = prs.Context(p)
+        ctx.set_initial(dev(u0))
+        ctx.coarse_sweep()
+        k, hist = ctx.iterate(50, 1e-9)
+        buf = torch.empty((p.n, p.n), dtype=torch.float64, device="cuda")
+        outs.append((k, hist, np.stack([host(ctx.get_slice(n, buf)).copy() for n in range(p.N + 1)])))
+        ctx.close()
+    (k1, h1, t1), (k2, h2, t2) = outs
+    assert k1 == k2 and h1 == h2 and np.array_equal(t1, t2)
+    assert k1 <= p.N and (h1[-1] <= 1e-9 or k1 == p.N)
+    assert all(h > 1e-9 for h in h1[:-1])
+    o = oracle.Oracle(p)
+    ctrajs, cupds = o.parareal(u0, 50, tol=1e-9)
+    assert len(cupds) == k1
+    scale = max(float(np.max(np.abs(t))) for t in ctrajs)
+    assert float(np.max(np.abs(t1 - ctrajs[-1]))) / scale <= TOL
+
+
+def test_non_finite_iterate_reports_divergence():
+    prs = prs_mod()
+    p = Problem(dim=2, n=16, N=4, s=2)
+    u0 = np.ones((16, 16))
+    u0[3, 4] = np.nan
+    ctx = prs.Context(p)
+    ctx.set_initial(dev(u0))
+    ctx.coarse_sweep()
+    ctx.fine_sweep()
+    with pytest.raises(prs.PrsError) as ei:
+        ctx.parareal_correct()
+    assert ei.value.code == prs.PRS_EDIVERGED
+
+
+def test_host_buffers_round_trip():
+    prs = prs_mod()
+    p = Problem(dim=2, n=33, source=1, N=3, s=2)
+    u0 = synth.initial_state(p)
+    ctx = prs.Context(p)
+    ctx.set_initial(np.ascontiguousarray(u0))
+    ctx.coarse_sweep()
+    out = np.zeros_like(u0)
+    ctx.get_slice(0, out)
+    assert np.array_equal(out, u0)
+    ctx.get_slice(3, out)
+    want = oracle.Oracle(p).coarse_sweep(u0)[3]
+    assert nerr(out, want, want) <= TOL
+
+
+# ------------------------------------------------------ full BASELINE sizes
+def test_c0_full_matches_modal_closed_form():
+    """P1 at full c0 size on the GPU: every iterate is a^k_n phi (scalar recurrence)."""
+    p = synth.CONFIGS["c0"]
+    u0 = synth.initial_state(p)
+    gtrajs, _ = gpu_parareal(p, u0, p.N)
+    lam = modal.lambdas((1, 1), p.n, p.c, 2)
+    sp = modal.ScalarParareal(lam, p.T, p.N, p.s, FIE, FIE, src_amp=2 * mp.pi ** 2 + p.c - 1)
+    want = sp.run(1, p.N)
+    for k in range(p.N + 1):
+        for n in range(p.N + 1):
+            assert nerr(gtrajs[k][n], float(want[k][n]) * u0, u0) <= TOL
+
+
+def test_c2_full_size_modal_property_two_iterations():
+    """c2 (128^3, N = 64, s = 32) on the GPU, k = 0, 1, 2: every iterate equals a^k_n phi_3D
+    with a^k_n from the scalar FIE-FIE parareal recurrence (P1 holds at any size)."""
+    p = synth.CONFIGS["c2"]
+    u0 = synth.initial_state(p)
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    ctx.set_initial(dev(u0))
+    ctx.coarse_sweep()
+    lam = modal.lambdas((1, 1, 1), p.n, p.c, 3)
+    sp = modal.ScalarParareal(lam, p.T, p.N, p.s, FIE, FIE, src_amp=3 * mp.pi ** 2 + p.c - 1)
+    want = sp.run(1, 2)
+    buf = torch.empty((p.n,) * 3, dtype=torch.float64, device="cuda")
+    du0 = dev(u0)
+    for k in range(3):
+        for n in (1, 2, 17, 40, 64):
+            got = ctx.get_slice(n, buf)
+            e = float(torch.max(torch.abs(got - float(want[k][n]) * du0)).item())
+            assert e <= TOL, (k, n, e)
+        if k < 2:
+            ctx.fine_sweep()
+            ctx.parareal_correct()
+    ctx.close()
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_full_size_single_steps(cfg):
+    """One coarse (tau = Delta T) and one fine (tau = delta t) step at the BASELINE size."""
+    p = synth.CONFIGS[cfg]
+    prs = prs_mod()
+    ctx = prs.Context(p.replace(N=1))
+    o = oracle.Oracle(p)
+    u = synth.initial_state(p.replace(init="modes" if p.dim == 2 else "phi", seed=5))
+    if p.dim == 3:
+        u = u + 0.01 * rand_field(p, 9)
+    du = dev(u)
+    out = torch.empty_like(du)
+    dT, dt = p.T / p.N, p.T / (p.N * p.s)
+    for sch, tau, tn in ((p.G, dT, 3 * dT), (p.F, dt, 17 * dt)):
+        ctx.step(sch, tau, tn, du, out)
+        want = o.step(sch, tau, tn, u)
+        assert nerr(host(out), want, want, u) <= TOL, (cfg, sch, tau)
+    ctx.close()
+
+
+def test_c3_full_size_batched_fine_step_sampled():
+    """c3 at full size in the bench's launch configuration: one batched fine step over all
+    64 slices (8 GiB), sampled slices checked against the oracle one by one."""
+    p = synth.CONFIGS["c3"]
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    base = synth.initial_state(p)
+    B = p.N
+    du = torch.empty((B, p.n, p.n), dtype=torch.float64, device="cuda")
+    dbase = dev(base)
+    for b in range(B):
+        du[b].copy_(dbase * (1.0 + b / B))
+    out = torch.empty_like(du)
+    j = 5
+    ctx.step_batch(1, 0, j, du, out, B)
+    o = oracle.Oracle(p)
+    dt = p.T / (p.N * p.s)
+    for b in (0, 37, 63):
+        u = base * (1.0 + b / B)
+        want = o.step(p.F, dt, float(b * p.s + j + 1) * dt, u)
+        assert nerr(host(out[b]), want, want, u) <= TOL, b
+    ctx.close()
+    del du, out
+    torch.cuda.empty_cache()
+
+
+def test_c1_full_size_first_iterations():
+    """c1 at full size (256^2, N = 32, s = 64, DR-DR): iterates k = 0, 1 against the oracle."""
+    p = synth.CONFIGS["c1"]
+    u0 = synth.initial_state(p)
+    o = oracle.Oracle(p)
+    ctrajs, _ = o.parareal(u0, 1, fixed=True)
+    gtrajs, _ = gpu_parareal(p, u0, 1)
+    for k in range(2):
+        scale = max(float(np.max(np.abs(u0))), float(np.max(np.abs(ctrajs[k]))))
+        assert float(np.max(np.abs(gtrajs[k] - ctrajs[k]))) / scale <= TOL, k
