@@ -5,7 +5,7 @@
 #include <string>
 
 #include "../../include/prs.h"
-#include "lines.cuh"
+#include "common.cuh"
 
 struct prs_ctx;
 int prs_internal_prof_begin(prs_ctx *ctx);

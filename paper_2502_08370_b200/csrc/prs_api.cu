@@ -16,7 +16,9 @@
 
 #include "../../include/prs.h"
 #include "dd.cuh"
-#include "lines.cuh"
+#include "lpass.cuh"
+#include "setup.cuh"
+#include "xpass.cuh"
 
 using namespace prs;
 
@@ -222,6 +224,7 @@ static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const dou
     a.nlines = B * a.lines_per_state;
     a.P = next_pow2((n + LCH - 1) / LCH);
     a.S = cpad_host(n);
+    a.St = cpad_host(n + 1);
     a.dim = dim;
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
@@ -239,7 +242,7 @@ static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const dou
     const int dr = (scheme == PRS_DR) ? 1 : 0;
     const int coef = ctx->p.coef_kind;
     const int src = ctx->p.source_kind;
-    size_t shm = sizeof(double) * (size_t)(1 + dr + coef) * lpb * a.S + sizeof(double2) * (threads / 32 + 1);
+    const size_t shm = sizeof(double) * xpass_smem_doubles(lpb, a.S, a.St, coef, threads);
     const long long blocks = (a.nlines + lpb - 1) / lpb;
     void (*kern)(XArgs) = nullptr;
 #define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass_kernel<C, D, S_>;
@@ -274,7 +277,9 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
         a.nq = n;
         a.Sq = n;
     }
-    a.nwb = (n + PW - 1) / PW;
+    const int coef = ctx->p.coef_kind;
+    const int PWc = coef ? 8 : 16;  // variable kappa stages pivots too: narrower panels, more CTAs/SM
+    a.nwb = (n + PWc - 1) / PWc;
     a.npanels = B * a.nq * a.nwb;
     int CL = 1;
     while ((n + CL - 1) / CL > 32 * LCH) CL *= 2;
@@ -286,6 +291,7 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
     a.R = (n + CL - 1) / CL;
     a.CP = next_pow2((a.R + LCH - 1) / LCH);
     a.S = cpad_host(a.R);
+    a.St = cpad_host(a.R + 1);
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
@@ -297,11 +303,10 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
     a.e_delta = ep.delta;
     a.e_traj = ep.traj;
     a.e_red = ctx->red;
-    const int coef = ctx->p.coef_kind;
-    const int threads = PW * a.CP;
-    size_t shm = sizeof(double) * (size_t)(1 + coef) * PW * a.S + sizeof(double2) * 2 * PW;
+    const int threads = PWc * a.CP;
+    const size_t shm = sizeof(double) * lpass_smem_doubles(PWc, a.S, a.St, coef);
     void (*kern)(LArgs) = nullptr;
-#define LK(C, E) if (coef == C && ep.kind == E) kern = lpass_kernel<C, E>;
+#define LK(C, E) if (coef == C && ep.kind == E) kern = lpass_kernel<(C ? 8 : 16), C, E>;
     LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
 #undef LK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -400,7 +405,7 @@ static int validate(const prs_problem *p, std::string &err) {
         err = "3-D Douglas-Rachford (M = 3) is not implemented on the GPU path";
         return PRS_EUNSUPPORTED;
     }
-    if (p->split == 0 && p->n > 8 * 32 * LCH) { err = "n too large for the line kernels"; return PRS_EUNSUPPORTED; }
+    if (p->split == 0 && p->n > 16 * 256) { err = "n > 4096 is not supported by the line kernels"; return PRS_EUNSUPPORTED; }
     return PRS_OK;
 }
 

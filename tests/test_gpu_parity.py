@@ -76,11 +76,15 @@ def test_single_step_parity(p):
     du = dev(u)
     out = torch.empty_like(du)
     schemes = (FIE, DR) if p.dim == 2 else (FIE,)
+    Au = o.apply(-1, u)
     for sch in schemes:
         for tau, tn in ((1e-4, 0.3), (0.37, 0.74)):
             ctx.step(sch, tau, tn, du, out)
             want = o.step(sch, tau, tn, u)
-            e = nerr(host(out), want, want, u)
+            # white-noise input: DR's explicit term tau A U_n is the largest intermediate, and
+            # rounding of both implementations scales with it (R1/R13)
+            scales = (want, u, tau * Au) if sch == DR else (want, u)
+            e = nerr(host(out), want, *scales)
             assert e <= TOL, (sch, tau, e)
     ctx.close()
 
