@@ -1,11 +1,38 @@
 // dd.cuh -- domain-decomposition (DD) splitting stage solves.
-// Placeholder until the strip-block solver lands: every entry reports PRS_EUNSUPPORTED.
+//
+// Colour j's stage matrix I - tau A_j is block diagonal with one block per connected strip of
+// its support (rho_j > 0) and identity rows elsewhere.  With
+// kappa = 1 and rho = rho(x) a block (W columns x n rows, U as a W x n matrix) reads
+//     (I - tau A_j) U = S U - tau R U Y,   S = I - tau X + tau c R,   R = diag(rho_j(x_i)),
+// X the rho_j-face-weighted 1-D operator in x and Y the 1-D Dirichlet second difference in y.
+// With the generalised eigenpairs S q_a = theta_a R q_a, Q^T R Q = I (precomputed once per
+// block and tau from the symmetric tridiagonal C = R^{-1/2} S R^{-1/2} by Jacobi rotations),
+// the block solve is exactly (up to rounding)
+//     G = Q^T F  ->  (theta_a I - tau Y) v_a = g_a  (n-long tridiagonal, one per mode a)
+//     ->  U = Q V.
+// One cluster of CL CTAs holds one block of one state in shared memory (R <= 128 rows per
+// CTA): two dense W x W transforms on the fp64 FMA pipes (register-tiled, Q streamed through
+// shared memory), and the n-long tridiagonal solves with the chunk-parallel Thomas of
+// common.cuh across the cluster (distributed shared memory).  This is the fp64-ALU-bound
+// kernel of the path (~4W flops per support point per stage).
+//
+// FIE step = stage 0 (colour 0) then stage 1 (colour 1), both in place in
+// the output buffer V:
+//   stage 0: r = U + tau F [DR: + w, w = tau A_1 U (colour-1 operator)], solve colour-0
+//            blocks, V = x [DR: - w]; points with rho_1 = 0 are final after this stage.
+//   stage 1: r = V where rho_0 > 0, else U + tau F (the identity rows of stage 0, where for
+//            DR the w terms cancel), solve colour-1 blocks, V = x.
+// The parareal epilogues (Delta, correction, initial guess) are fused into the stores of
+// the final values of each stage.
 #pragma once
 #include <cuda_runtime.h>
+
 #include <string>
+#include <vector>
 
 #include "../../include/prs.h"
 #include "common.cuh"
+#include "lpass.cuh"
 
 struct prs_ctx;
 int prs_internal_prof_begin(prs_ctx *ctx);
@@ -13,25 +40,750 @@ int prs_internal_prof_end(prs_ctx *ctx, int kind, double bytes);
 
 namespace prs {
 
-struct DDData {
-    const double *sinpi = nullptr;
+constexpr int DD_RMAX = 128;   // rows per CTA
+constexpr int DD_WMAX = 152;   // widest block
+constexpr int DD_WPAD = 164;   // shared row stride of a tile (>= DD_WMAX, == 4 mod 16)
+constexpr int DD_CWMAX = 19;   // columns per GEMM thread, ceil(DD_WMAX / 8)
+constexpr int DD_KC = 16;      // Q rows staged per k-chunk
+constexpr int DD_THREADS = 256;
+
+// ------------------------------------------------------------- partition of unity --
+// rho_0 at a 1-based position xpos (integer = node, half-integer = face), index-space
+// geometry of DESIGN.md R6: S strips of w = n/S nodes, interface m at w m + 1/2, ramp of
+// width beta = ov centred on it; colour 0 = even strips.  rho_1 = 1 - rho_0.
+__device__ inline double dd_ramp_down(double xpos, double xl, int ov, int cosine) {
+    const double u = (xpos - xl) / (double)ov;
+    if (u <= 0.0) return 1.0;
+    if (u >= 1.0) return 0.0;
+    if (cosine) return 0.5 * (1.0 + cos(3.14159265358979323846 * u));
+    return 1.0 - u;
+}
+__device__ inline double dd_rho0(double xpos, int n, int S, int ov, int cosine) {
+    const int w = n / S;
+    int k = (int)floor((xpos - 0.5) / (double)w);
+    k = max(0, min(S - 1, k));
+    const double half = 0.5 * (double)ov;
+    if (k + 1 <= S - 1) {
+        const double xi = (double)(w * (k + 1)) + 0.5;
+        if (xpos > xi - half) {
+            const double d = dd_ramp_down(xpos, xi - half, ov, cosine);
+            return (k % 2 == 0) ? d : 1.0 - d;
+        }
+    }
+    if (k >= 1) {
+        const double xi = (double)(w * k) + 0.5;
+        if (xpos < xi + half) {
+            const double d = dd_ramp_down(xpos, xi - half, ov, cosine);
+            return ((k - 1) % 2 == 0) ? d : 1.0 - d;
+        }
+    }
+    return (k % 2 == 0) ? 1.0 : 0.0;
+}
+// rhon[j*n + i] = rho_j(node i+1), rhof[j*(n+1) + f] = rho_j(face f + 1/2)
+__global__ void dd_rho_tables(int n, int S, int ov, int cosine, double *rhon, double *rhof) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double r = dd_rho0((double)(i + 1), n, S, ov, cosine);
+        rhon[i] = r;
+        rhon[n + i] = 1.0 - r;
+    }
+    if (i <= n) {
+        const double r = dd_rho0((double)i + 0.5, n, S, ov, cosine);
+        rhof[i] = r;
+        rhof[n + 1 + i] = 1.0 - r;
+    }
+}
+
+// -------------------------------------------------------- per-block factorisation --
+// Symmetric tridiagonal C = R^{-1/2} S R^{-1/2} of block (colour j, columns i0..i0+W-1):
+//   S_ii = 1 + tau h^-2 (rho(i-1/2) + rho(i+1/2)) + tau c rho(i),  S_i,i+1 = -tau h^-2 rho(i+1/2)
+// then cyclic Jacobi (parallel round-robin pairs) on C in shared memory, eigenvectors in
+// global memory; Q = R^{-1/2} Z, QT = Q^T, theta, and the pivots of theta_a I - tau Y.
+struct DDBlock {
+    int colour, i0, W;
+    double *Q = nullptr, *QT = nullptr, *theta = nullptr, *idy = nullptr;  // per tau slot
 };
 
-inline int dd_init(DDData &, const prs_problem &, double, double, cudaStream_t, std::string &err) {
-    err = "DD splitting is not implemented on the GPU path yet";
-    return PRS_EUNSUPPORTED;
+__global__ void __launch_bounds__(DD_THREADS) dd_factor_kernel(int n, int i0, int W, const double *rhon,
+                                                               const double *rhof, double tau, double h2inv,
+                                                               double c, double *Z, double *Q, double *QT,
+                                                               double *theta, double *idy, int sweeps) {
+    extern __shared__ double sh[];
+    double *C = sh;                 // W x W (row stride W)
+    double *cs = sh + W * W;        // rotation cos per pair
+    double *sn = cs + DD_WMAX / 2 + 1;
+    int *pp = reinterpret_cast<int *>(sn + DD_WMAX / 2 + 1);
+    int *qq = pp + DD_WMAX / 2 + 1;
+    const int tid = threadIdx.x;
+    // assemble C and Z = I
+    for (int e = tid; e < W * W; e += blockDim.x) {
+        const int r = e / W, k = e % W;
+        const int gi = i0 + r;  // 0-based node index
+        const double rr = rhon[gi];
+        double v = 0.0;
+        if (r == k) {
+            v = (1.0 + tau * h2inv * (rhof[gi] + rhof[gi + 1]) + tau * c * rr) / rr;
+        } else if (k == r + 1) {
+            v = -tau * h2inv * rhof[gi + 1] / sqrt(rr * rhon[gi + 1]);
+        } else if (r == k + 1) {
+            v = -tau * h2inv * rhof[gi] / sqrt(rr * rhon[gi - 1]);
+        }
+        C[e] = v;
+        Z[e] = (r == k) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // round-robin pairing over Wp = W rounded up to even (a dummy index when W is odd)
+    const int Wp = W + (W & 1);
+    const int npair = Wp / 2;
+    for (int sw = 0; sw < sweeps; ++sw) {
+        for (int round = 0; round < Wp - 1; ++round) {
+            if (tid < npair) {
+                // circle method: pair k of round r is (r+k, r-k) mod (Wp-1), pair 0 is (r, Wp-1);
+                // every index appears once per round and every pair once per sweep
+                const int k = tid;
+                const int a = (round + k) % (Wp - 1);
+                const int b = (k == 0) ? (Wp - 1) : (round - k + Wp - 1) % (Wp - 1);
+                int p = min(a, b), q = max(a, b);
+                double cc = 1.0, ss = 0.0;
+                if (q < W && p != q) {
+                    const double apq = C[p * W + q];
+                    if (apq != 0.0) {
+                        const double app = C[p * W + p], aqq = C[q * W + q];
+                        const double th = (aqq - app) / (2.0 * apq);
+                        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                        cc = 1.0 / sqrt(t * t + 1.0);
+                        ss = t * cc;
+                    }
+                } else {
+                    p = q = -1;
+                }
+                pp[tid] = p;
+                qq[tid] = q;
+                cs[tid] = cc;
+                sn[tid] = ss;
+            }
+            __syncthreads();
+            // rows: C <- J^T C  (each pair mixes rows p, q)
+            for (int e = tid; e < npair * W; e += blockDim.x) {
+                const int k = e / W, col = e % W;
+                const int p = pp[k], q = qq[k];
+                if (p < 0) continue;
+                const double cc = cs[k], ss = sn[k];
+                const double xp = C[p * W + col], xq = C[q * W + col];
+                C[p * W + col] = cc * xp - ss * xq;
+                C[q * W + col] = ss * xp + cc * xq;
+            }
+            __syncthreads();
+            // columns: C <- C J, Z <- Z J
+            for (int e = tid; e < npair * W; e += blockDim.x) {
+                const int k = e / W, row = e % W;
+                const int p = pp[k], q = qq[k];
+                if (p < 0) continue;
+                const double cc = cs[k], ss = sn[k];
+                const double xp = C[row * W + p], xq = C[row * W + q];
+                C[row * W + p] = cc * xp - ss * xq;
+                C[row * W + q] = ss * xp + cc * xq;
+                const double zp = Z[row * W + p], zq = Z[row * W + q];
+                Z[row * W + p] = cc * zp - ss * zq;
+                Z[row * W + q] = ss * zp + cc * zq;
+            }
+            __syncthreads();
+        }
+    }
+    // eigenvalues on the diagonal; Q = R^{-1/2} Z; pivots of theta_a + 2 s, off -s (s = tau/h^2)
+    const double s = tau * h2inv;
+    for (int a = tid; a < W; a += blockDim.x) {
+        const double th = C[a * W + a];
+        theta[a] = th;
+        const double bd = th + 2.0 * s;
+        double d = bd;
+        for (int l = 0; l < n; ++l) {
+            if (l > 0) d = bd - s * s / d;
+            idy[(long long)l * W + a] = 1.0 / d;
+        }
+    }
+    for (int e = tid; e < W * W; e += blockDim.x) {
+        const int r = e / W, k = e % W;
+        const double q = Z[e] / sqrt(rhon[i0 + r]);
+        Q[e] = q;             // Q[i][a]
+        QT[k * W + r] = q;    // QT[a][i]
+    }
 }
-inline int dd_factors(DDData &, int, double, cudaStream_t, std::string &err) {
-    err = "DD splitting is not implemented on the GPU path yet";
-    return PRS_EUNSUPPORTED;
+
+// ------------------------------------------------------------------ stage kernel ---
+struct DDStageArgs {
+    const double *U;     // step input (batch)
+    double *V;           // step output (batch), stage 1 reads it too
+    long long vol;
+    int n, B;
+    int stage;           // 0 or 1 (colour)
+    int CL, R;           // cluster size, rows per CTA
+    int nblk;            // blocks of this colour
+    const int *bi0, *bW; // block column start / width
+    const double *const *Q, *const *QT, *const *idy;  // per block
+    double tau, h2inv, c;
+    const double *rhon, *rhof;  // rho tables (colour 0 then colour 1)
+    double src_amp;
+    const double *sinpi;
+    TimeArgs ta;
+    int epi;
+    const double *e_gc;
+    double *e_gcache;
+    const double *e_delta;
+    double *e_traj;
+    unsigned long long *e_red;
+};
+
+// GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place.
+__device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
+    const int tid = threadIdx.x;
+    const int rg = tid >> 3, cg = tid & 7;
+    const int CW = (W + 7) >> 3;
+    double acc[4][DD_CWMAX];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < DD_CWMAX; ++j) acc[r][j] = 0.0;
+    for (int k0 = 0; k0 < W; k0 += DD_KC) {
+        const int kc = min(DD_KC, W - k0);
+        __syncthreads();  // previous chunk consumed
+        for (int e = tid; e < kc * W; e += blockDim.x) Ms[(e / W) * DD_WPAD + (e % W)] = __ldg(M + (long long)k0 * W + e);
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            double f[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int l = rg + 32 * r;
+                f[r] = (l < nrow) ? T[cpad(l) * DD_WPAD + k0 + kk] : 0.0;
+            }
+            const double *mrow = Ms + kk * DD_WPAD + cg * CW;
+#pragma unroll
+            for (int j = 0; j < DD_CWMAX; ++j) {
+                if (j < CW) {
+                    const double m = mrow[j];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc[r][j] = fma(f[r], m, acc[r][j]);
+                }
+            }
+        }
+    }
+    __syncthreads();  // all reads of T done before the in-place write
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int l = rg + 32 * r;
+        if (l < nrow) {
+#pragma unroll
+            for (int j = 0; j < DD_CWMAX; ++j) {
+                const int col = cg * CW + j;
+                if (j < CW && col < W) T[cpad(l) * DD_WPAD + col] = acc[r][j];
+            }
+        }
+    }
+    __syncthreads();
 }
-template <class Fac>
-inline int dd_step(DDData &, int, double, Fac *, const double *, double *, long long, const TimeArgs &, int,
-                   const double *, double *, const double *, double *, unsigned long long *, cudaStream_t,
-                   prs_ctx *, std::string &err, long long &) {
-    err = "DD splitting is not implemented on the GPU path yet";
-    return PRS_EUNSUPPORTED;
+
+template <int DR, int SRC>
+__global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
+    extern __shared__ double sh[];
+    double *T = sh;                                          // (cpad(R-1)+1) x DD_WPAD
+    double *Ms = sh + (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // DD_KC x DD_WPAD
+    double2 *sc = reinterpret_cast<double2 *>(Ms + DD_KC * DD_WPAD);  // 8 x DD_WMAX chunk maps
+    double2 *ctf = sc + 8 * DD_WMAX;                          // cluster totals fwd
+    double2 *ctb = ctf + DD_WMAX;                             // cluster totals bwd
+    __shared__ double sdmax;
+    __shared__ unsigned long long sbad;
+
+    const int tid = threadIdx.x;
+    const int crank = (a.CL > 1) ? (int)cg::this_cluster().block_rank() : 0;
+    const long long task = blockIdx.x / a.CL;
+    const int blk = (int)(task % a.nblk);
+    const long long b = task / a.nblk;
+    const int i0 = a.bi0[blk], W = a.bW[blk];
+    const int n = a.n;
+    const int r0 = crank * a.R;
+    const int nrow = max(0, min(a.R, n - r0));
+    const double *Ub = a.U + b * a.vol;
+    double *Vb = a.V + b * a.vol;
+    const int me = a.stage, other = 1 - a.stage;
+    const double *rn_me = a.rhon + me * n, *rf_me = a.rhof + me * (n + 1);
+    const double *rn_ot = a.rhon + other * n, *rf_ot = a.rhof + other * (n + 1);
+    if (tid == 0) {
+        sdmax = 0.0;
+        sbad = 0;
+    }
+    double ampt = 0.0;
+    if (SRC) ampt = a.src_amp * exp(-src_time(a.ta, b));
+
+    // ---- load the right-hand side tile ----
+    for (int e = tid; e < nrow * W; e += blockDim.x) {
+        const int rl = e / W, ci = e % W;
+        const int l = r0 + rl, i = i0 + ci;
+        const long long g = (long long)l * n + i;
+        double r;
+        if (me == 0) {
+            const double u = Ub[g];
+            r = u;
+            if (SRC) r += a.tau * (ampt * a.sinpi[i] * a.sinpi[l]);
+            if (DR) {  // w = tau A_1 U (colour-1 operator) at (i, l)
+                const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
+                const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
+                const double rnode = rn_ot[i];
+                const double w = a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) +
+                                           rnode * (vp - 2.0 * u + vm)) * a.h2inv - rnode * a.c * u);
+                r += w;
+            }
+        } else {
+            if (rn_ot[i] > 0.0) {
+                r = Vb[g];
+            } else {
+                r = Ub[g];
+                if (SRC) r += a.tau * (ampt * a.sinpi[i] * a.sinpi[l]);
+            }
+        }
+        T[cpad(rl) * DD_WPAD + ci] = r;
+    }
+    // ---- G = F Q ----
+    dd_tile_gemm(T, a.Q[blk], W, nrow, Ms);
+
+    // ---- (theta_a I - tau Y) v_a = g_a along y: warp = chunk t, lanes = modes ----
+    const int t = tid >> 5, lane = tid & 31;
+    const int e0 = t * LCH;
+    const int cnt = max(0, min(LCH, nrow - e0));
+    const double ms = -a.tau * a.h2inv;  // off-diagonal of theta I - tau Y
+    const double *idy = a.idy[blk];
+    constexpr int NMR = (DD_WMAX + 31) / 32;
+    double Ain[NMR], Bin[NMR];
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) {
+        const int am = lane + 32 * rr;
+        double A = 1.0, B = 0.0;
+        if (am < W) {
+#pragma unroll
+            for (int i = 0; i < LCH; ++i)
+                if (i < cnt) {
+                    const int l = r0 + e0 + i;
+                    const double m = (l > 0) ? ms * __ldg(idy + (long long)(l - 1) * W + am) : 0.0;
+                    B = fma(-m, B, T[cpad(e0 + i) * DD_WPAD + am]);
+                    A = -m * A;
+                }
+            sc[t * DD_WMAX + am] = make_double2(A, B);
+        }
+        Ain[rr] = A;
+        Bin[rr] = B;
+    }
+    __syncthreads();
+    const int nch = (nrow + LCH - 1) / LCH;
+    double yin[NMR];
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) {
+        const int am = lane + 32 * rr;
+        double EA = 1.0, EB = 0.0, TA = 1.0, TB = 0.0;  // exclusive prefix, CTA total
+        if (am < W) {
+            for (int q = 0; q < nch; ++q) {
+                const double2 v = sc[q * DD_WMAX + am];
+                if (q == t) {
+                    EA = TA;
+                    EB = TB;
+                }
+                TB = fma(v.x, TB, v.y);
+                TA = v.x * TA;
+            }
+            if (t >= nch) {
+                EA = TA;
+                EB = TB;
+            }
+            if (t == 0) ctf[am] = make_double2(TA, TB);
+        }
+        Ain[rr] = EA;
+        Bin[rr] = EB;
+    }
+    double Ycta[NMR];
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) Ycta[rr] = 0.0;
+    if (a.CL > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+#pragma unroll
+        for (int rr = 0; rr < NMR; ++rr) {
+            const int am = lane + 32 * rr;
+            if (am < W)
+                for (int r = 0; r < crank; ++r) {
+                    const double2 v = cl.map_shared_rank(ctf, r)[am];
+                    Ycta[rr] = fma(v.x, Ycta[rr], v.y);
+                }
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) yin[rr] = fma(Ain[rr], Ycta[rr], Bin[rr]);
+    __syncthreads();
+    // F3 + backward composition
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) {
+        const int am = lane + 32 * rr;
+        if (am < W) {
+            double y = yin[rr], Pb = 1.0, Qb = 0.0;
+#pragma unroll
+            for (int i = 0; i < LCH; ++i)
+                if (i < cnt) {
+                    const int l = r0 + e0 + i;
+                    const double m = (l > 0) ? ms * __ldg(idy + (long long)(l - 1) * W + am) : 0.0;
+                    const double id = __ldg(idy + (long long)l * W + am);
+                    const double ccv = (l < n - 1) ? ms * id : 0.0;
+                    double *p = T + cpad(e0 + i) * DD_WPAD + am;
+                    y = fma(-m, y, *p);
+                    *p = y;
+                    Qb = fma(Pb * id, y, Qb);
+                    Pb *= -ccv;
+                }
+            sc[t * DD_WMAX + am] = make_double2(Pb, Qb);
+        }
+    }
+    __syncthreads();
+    double xin[NMR];
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) {
+        const int am = lane + 32 * rr;
+        double EP = 1.0, EQ = 0.0, TP = 1.0, TQ = 0.0;
+        if (am < W) {
+            for (int q = nch - 1; q >= 0; --q) {
+                const double2 v = sc[q * DD_WMAX + am];
+                if (q == t) {
+                    EP = TP;
+                    EQ = TQ;
+                }
+                TQ = fma(v.x, TQ, v.y);
+                TP = v.x * TP;
+            }
+            if (t >= nch) {
+                EP = 1.0;
+                EQ = 0.0;
+            }
+            if (t == 0) ctb[am] = make_double2(TP, TQ);
+        }
+        Ain[rr] = EP;
+        Bin[rr] = EQ;
+    }
+    double Xcta[NMR];
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) Xcta[rr] = 0.0;
+    if (a.CL > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+#pragma unroll
+        for (int rr = 0; rr < NMR; ++rr) {
+            const int am = lane + 32 * rr;
+            if (am < W)
+                for (int r = a.CL - 1; r > crank; --r) {
+                    const double2 v = cl.map_shared_rank(ctb, r)[am];
+                    Xcta[rr] = fma(v.x, Xcta[rr], v.y);
+                }
+        }
+        cl.sync();
+    }
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) xin[rr] = fma(Ain[rr], Xcta[rr], Bin[rr]);
+    // B3
+#pragma unroll
+    for (int rr = 0; rr < NMR; ++rr) {
+        const int am = lane + 32 * rr;
+        if (am < W) {
+            double x = xin[rr];
+#pragma unroll
+            for (int i = LCH - 1; i >= 0; --i)
+                if (i < cnt) {
+                    const int l = r0 + e0 + i;
+                    const double id = __ldg(idy + (long long)l * W + am);
+                    const double ccv = (l < n - 1) ? ms * id : 0.0;
+                    double *p = T + cpad(e0 + i) * DD_WPAD + am;
+                    x = fma(id, *p, -ccv * x);
+                    *p = x;
+                }
+        }
+    }
+    // ---- U = V Q^T ----
+    dd_tile_gemm(T, a.QT[blk], W, nrow, Ms);
+
+    // ---- store (+ fused parareal epilogue for final values) ----
+    double dmax = 0.0;
+    unsigned long long bad = 0;
+    for (int e = tid; e < nrow * W; e += blockDim.x) {
+        const int rl = e / W, ci = e % W;
+        const int l = r0 + rl, i = i0 + ci;
+        const long long g = (long long)l * n + i;
+        double x = T[cpad(rl) * DD_WPAD + ci];
+        if (DR && me == 0) {  // V = x - w
+            const double u = Ub[g];
+            const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
+            const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
+            const double rnode = rn_ot[i];
+            x -= a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) + rnode * (vp - 2.0 * u + vm)) * a.h2inv -
+                          rnode * a.c * u);
+        }
+        const bool final_here = (me == 1) || !(rn_ot[i] > 0.0);
+        const int ep = final_here ? a.epi : EPI_STORE;
+        const long long gb = b * a.vol + g;
+        if (ep == EPI_STORE) {
+            Vb[g] = x;
+        } else if (ep == EPI_DELTA) {
+            Vb[g] = x - a.e_gc[gb];
+        } else if (ep == EPI_CORRECT) {
+            const double nv = x + a.e_delta[g];
+            const double ov = a.e_traj[g];
+            a.e_gcache[g] = x;
+            a.e_traj[g] = nv;
+            dmax = fmax(dmax, fabs(nv - ov));
+            if (!isfinite(nv)) bad = 1;
+        } else {  // INIT
+            a.e_gcache[g] = x;
+            a.e_traj[g] = x;
+        }
+    }
+    if (a.epi == EPI_CORRECT) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, off);
+        }
+        if (lane == 0) {
+            atomicMax(a.e_red, (unsigned long long)__double_as_longlong(dmax));
+            if (bad) atomicOr(a.e_red + 1, 1ull);
+        }
+    }
+    (void)rn_me;
+    (void)rf_me;
+    (void)rf_me;
 }
-inline void dd_free(DDData &) {}
+
+inline size_t dd_stage_smem_bytes() {
+    return sizeof(double) * ((size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD + DD_KC * DD_WPAD) +
+           sizeof(double2) * (8 * DD_WMAX + 2 * DD_WMAX);
+}
+
+// ------------------------------------------------------------------ host side ------
+struct DDData {
+    const double *sinpi = nullptr;
+    int n = 0, S = 0, ov = 0, ramp = 0, dim = 2;
+    double c = 0, h2inv = 0;
+    double *rhon = nullptr, *rhof = nullptr, *Z = nullptr;
+    std::vector<int> bi0[2], bW[2];
+    int *d_bi0[2] = {nullptr, nullptr}, *d_bW[2] = {nullptr, nullptr};
+    // per tau slot (3) and colour (2): device arrays of per-block pointers + the storage
+    double tau[3] = {-1.0, -1.0, -1.0};
+    std::vector<double *> store[3];
+    const double **d_Q[3][2] = {}, **d_QT[3][2] = {}, **d_idy[3][2] = {};
+};
+
+// block extents from the index-space geometry (host; integers only, R6)
+inline void dd_blocks(int n, int S, int ov, int colour, std::vector<int> &i0, std::vector<int> &W) {
+    const int w = n / S, half = ov / 2;
+    i0.clear();
+    W.clear();
+    for (int k = colour; k < S; k += 2) {
+        // nodes (0-based) with rho > 0: strip k interior plus the ramps (half nodes each side)
+        int lo = k * w - (k > 0 ? half : 0);
+        int hi = (k + 1) * w - 1 + (k < S - 1 ? half : 0);
+        i0.push_back(lo);
+        W.push_back(hi - lo + 1);
+    }
+}
+
+inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cudaStream_t st, std::string &err) {
+    (void)h;
+    if (p.coef_kind != 0) {
+        err = "DD splitting on the GPU path supports kappa = 1 only";
+        return PRS_EUNSUPPORTED;
+    }
+    d.n = p.n;
+    d.S = p.dd_strips;
+    d.ov = p.dd_overlap;
+    d.ramp = p.dd_ramp;
+    d.c = p.c;
+    d.h2inv = h2inv;
+    if (d.S < 2 || d.ov < 2) {
+        err = "DD GPU path needs at least 2 strips and an overlap of at least 2 cells";
+        return PRS_EUNSUPPORTED;
+    }
+    if ((d.n + DD_RMAX - 1) / DD_RMAX > 8) {
+        err = "DD GPU path supports n <= 1024";
+        return PRS_EUNSUPPORTED;
+    }
+    for (int col = 0; col < 2; ++col) {
+        dd_blocks(d.n, d.S, d.ov, col, d.bi0[col], d.bW[col]);
+        for (int w : d.bW[col])
+            if (w > DD_WMAX) {
+                err = "DD block wider than " + std::to_string(DD_WMAX) + " columns";
+                return PRS_EUNSUPPORTED;
+            }
+    }
+    if (cudaMalloc(&d.rhon, sizeof(double) * 2 * d.n) != cudaSuccess ||
+        cudaMalloc(&d.rhof, sizeof(double) * 2 * (d.n + 1)) != cudaSuccess ||
+        cudaMalloc(&d.Z, sizeof(double) * DD_WMAX * DD_WMAX) != cudaSuccess) {
+        err = "cudaMalloc (DD tables) failed";
+        return PRS_ECUDA;
+    }
+    dd_rho_tables<<<(d.n + 1 + 255) / 256, 256, 0, st>>>(d.n, d.S, d.ov, d.ramp, d.rhon, d.rhof);
+    for (int col = 0; col < 2; ++col) {
+        const size_t nb = d.bi0[col].size();
+        if (cudaMalloc(&d.d_bi0[col], sizeof(int) * nb) != cudaSuccess ||
+            cudaMalloc(&d.d_bW[col], sizeof(int) * nb) != cudaSuccess) {
+            err = "cudaMalloc (DD blocks) failed";
+            return PRS_ECUDA;
+        }
+        cudaMemcpyAsync(d.d_bi0[col], d.bi0[col].data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d.d_bW[col], d.bW[col].data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st);
+    }
+    cudaStreamSynchronize(st);
+    if (cudaGetLastError() != cudaSuccess) {
+        err = "DD table setup failed";
+        return PRS_ECUDA;
+    }
+    return PRS_OK;
+}
+
+inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::string &err) {
+    if (d.tau[slot] == tau) return PRS_OK;
+    for (double *p : d.store[slot]) cudaFree(p);
+    d.store[slot].clear();
+    d.tau[slot] = tau;
+    const size_t fsm = sizeof(double) * ((size_t)DD_WMAX * DD_WMAX + 2 * (DD_WMAX / 2 + 1)) +
+                       sizeof(int) * 2 * (DD_WMAX / 2 + 1);
+    if (cudaFuncSetAttribute(dd_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) !=
+        cudaSuccess) {
+        err = "cudaFuncSetAttribute(dd_factor_kernel) failed";
+        return PRS_ECUDA;
+    }
+    for (int col = 0; col < 2; ++col) {
+        const size_t nb = d.bi0[col].size();
+        std::vector<const double *> hQ(nb), hQT(nb), hI(nb);
+        for (size_t k = 0; k < nb; ++k) {
+            const int W = d.bW[col][k];
+            double *Q, *QT, *th, *idy;
+            if (cudaMalloc(&Q, sizeof(double) * W * W) != cudaSuccess ||
+                cudaMalloc(&QT, sizeof(double) * W * W) != cudaSuccess ||
+                cudaMalloc(&th, sizeof(double) * W) != cudaSuccess ||
+                cudaMalloc(&idy, sizeof(double) * (size_t)W * d.n) != cudaSuccess) {
+                err = "cudaMalloc (DD factors) failed";
+                return PRS_ECUDA;
+            }
+            d.store[slot].insert(d.store[slot].end(), {Q, QT, th, idy});
+            dd_factor_kernel<<<1, DD_THREADS, fsm, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
+                                                         d.rhof + col * (d.n + 1), tau, d.h2inv, d.c, d.Z, Q, QT,
+                                                         th, idy, 14);
+            hQ[k] = Q;
+            hQT[k] = QT;
+            hI[k] = idy;
+        }
+        const double **dq, **dqt, **di;
+        if (cudaMalloc(&dq, sizeof(double *) * nb) != cudaSuccess ||
+            cudaMalloc(&dqt, sizeof(double *) * nb) != cudaSuccess ||
+            cudaMalloc(&di, sizeof(double *) * nb) != cudaSuccess) {
+            err = "cudaMalloc (DD pointer tables) failed";
+            return PRS_ECUDA;
+        }
+        d.store[slot].insert(d.store[slot].end(), {(double *)dq, (double *)dqt, (double *)di});
+        cudaMemcpyAsync(dq, hQ.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(dqt, hQT.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(di, hI.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+        d.d_Q[slot][col] = dq;
+        d.d_QT[slot][col] = dqt;
+        d.d_idy[slot][col] = di;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+        err = "DD factorisation failed";
+        return PRS_ECUDA;
+    }
+    return PRS_OK;
+}
+
+inline void dd_free(DDData &d) {
+    for (auto &v : d.store) {
+        for (double *p : v) cudaFree(p);
+        v.clear();
+    }
+    double *bufs[] = {d.rhon, d.rhof, d.Z};
+    for (double *p : bufs)
+        if (p) cudaFree(p);
+    for (int c = 0; c < 2; ++c) {
+        if (d.d_bi0[c]) cudaFree(d.d_bi0[c]);
+        if (d.d_bW[c]) cudaFree(d.d_bW[c]);
+    }
+}
+
+// one DD step (two colour stages) on B states: in -> out
+inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *out, long long B, const TimeArgs &ta,
+                   int epi, const double *gc, double *gcache, const double *delta, double *traj,
+                   unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err, long long &launches,
+                   double src_amp, int src) {
+    const int n = d.n;
+    const int CL = (n + DD_RMAX - 1) / DD_RMAX;
+    const size_t shm = dd_stage_smem_bytes();
+    for (int stage = 0; stage < 2; ++stage) {
+        DDStageArgs a{};
+        a.U = in;
+        a.V = out;
+        a.vol = (long long)n * n;
+        a.n = n;
+        a.B = (int)B;
+        a.stage = stage;
+        a.CL = CL;
+        a.R = (n + CL - 1) / CL;
+        a.nblk = (int)d.bi0[stage].size();
+        a.bi0 = d.d_bi0[stage];
+        a.bW = d.d_bW[stage];
+        a.Q = d.d_Q[slot][stage];
+        a.QT = d.d_QT[slot][stage];
+        a.idy = d.d_idy[slot][stage];
+        a.tau = d.tau[slot];
+        a.h2inv = d.h2inv;
+        a.c = d.c;
+        a.rhon = d.rhon;
+        a.rhof = d.rhof;
+        a.src_amp = src_amp;
+        a.sinpi = d.sinpi;
+        a.ta = ta;
+        a.epi = epi;
+        a.e_gc = gc;
+        a.e_gcache = gcache;
+        a.e_delta = delta;
+        a.e_traj = traj;
+        a.e_red = red;
+        void (*kern)(DDStageArgs) = nullptr;
+        const int dr = scheme == PRS_DR;
+        if (dr && src) kern = dd_stage_kernel<1, 1>;
+        else if (dr) kern = dd_stage_kernel<1, 0>;
+        else if (src) kern = dd_stage_kernel<0, 1>;
+        else kern = dd_stage_kernel<0, 0>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess) {
+            err = "cudaFuncSetAttribute(dd_stage_kernel) failed";
+            return PRS_ECUDA;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(B * a.nblk * CL));
+        cfg.blockDim = dim3(DD_THREADS);
+        cfg.dynamicSmemBytes = shm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (prof && prs_internal_prof_begin(prof) != PRS_OK) return PRS_ECUDA;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+        launches++;
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
+            err = std::string("dd_stage_kernel: ") + cudaGetErrorString(e);
+            return PRS_ECUDA;
+        }
+        if (prof) {
+            long long cols = 0;
+            for (int w : d.bW[stage]) cols += w;
+            // algorithmic bytes: read + write of the block's support points
+            if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * cols * n * 16.0) != PRS_OK) return PRS_ECUDA;
+        }
+    }
+    return PRS_OK;
+}
 
 }  // namespace prs

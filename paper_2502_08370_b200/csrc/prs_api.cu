@@ -339,9 +339,9 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
 static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
                     long long B, const TimeArgs &ta, const EpiArgs &ep, bool prof) {
     if (ctx->p.split == 1)
-        return dd_step(ctx->dd, scheme, f.tau, ctx->fac, in, out, B, ta, ep.kind, ep.gc, ep.gcache,
-                       ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err,
-                       ctx->launches);
+        return dd_step(ctx->dd, scheme, (int)(&f - ctx->fac), in, out, B, ta, ep.kind, ep.gc, ep.gcache,
+                       ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err, ctx->launches,
+                       2.0 * M_PI * M_PI + ctx->p.c - 1.0, ctx->p.source_kind);
     TRY(launch_xpass(ctx, scheme, f, in, out, B, ta, prof));
     if (ctx->p.dim == 2) return launch_lpass(ctx, 1, f, out, out, B, ep, prof);
     EpiArgs st;

@@ -126,6 +126,37 @@ def test_batched_step_parity(p):
     ctx.close()
 
 
+# ----------------------------------------------------------- DD stage solves
+DD_STEP_CASES = [
+    Problem(dim=2, n=32, c=1.0, split=1, dd_strips=4, dd_overlap=4, dd_ramp=0, N=4, s=3),
+    Problem(dim=2, n=32, c=1.0, split=1, dd_strips=4, dd_overlap=4, dd_ramp=1, source=1, N=4, s=3),
+    Problem(dim=2, n=64, c=2.0, split=1, dd_strips=8, dd_overlap=2, dd_ramp=0, source=1, N=4, s=3),
+    Problem(dim=2, n=256, c=1.0, split=1, dd_strips=8, dd_overlap=8, dd_ramp=0, source=1, N=4, s=3),
+    Problem(dim=2, n=300, c=1.0, split=1, dd_strips=3, dd_overlap=6, dd_ramp=1, source=0, N=4, s=3),
+]
+
+
+@pytest.mark.parametrize("p", DD_STEP_CASES, ids=lambda p: f"n{p.n}_S{p.dd_strips}_b{p.dd_overlap}_r{p.dd_ramp}")
+def test_dd_single_step_parity(p):
+    """DD stage solves (separable eigen-transform + cluster tridiagonal) vs the oracle's band
+    elimination, FIE and DR, small and large tau."""
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    o = oracle.Oracle(p)
+    u = rand_field(p, 5 + p.n)
+    du = dev(u)
+    out = torch.empty_like(du)
+    Au = o.apply(-1, u)
+    for sch in (FIE, DR):
+        for tau, tn in ((1e-4, 0.3), (0.37, 0.74)):
+            ctx.step(sch, tau, tn, du, out)
+            want = o.step(sch, tau, tn, u)
+            scales = (want, u, tau * Au) if sch == DR else (want, u)
+            e = nerr(host(out), want, *scales)
+            assert e <= TOL, (sch, tau, e)
+    ctx.close()
+
+
 # ------------------------------------------------------- whole parareal runs
 def gpu_parareal(p, u0, K):
     """Run coarse sweep + K iterations; return per-k trajectories and updates."""
@@ -155,6 +186,11 @@ PARAREAL_CASES = [
     Problem(dim=3, n=20, c=1.0, source=1, N=5, s=4, G=FIE, F=FIE),                  # c2 recipe
     Problem(dim=2, n=37, c=1.0, source=1, N=5, s=3, G=DR, F=FIE),
     Problem(dim=2, n=37, c=1.0, source=1, N=5, s=3, G=FIE, F=DR),
+    # c4 recipe (DD, 8 strips, linear ramp), all four pairings (R12)
+    Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=5, s=4, G=FIE, F=FIE),
+    Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=5, s=4, G=FIE, F=DR),
+    Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=5, s=4, G=DR, F=FIE),
+    Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=5, s=4, G=DR, F=DR),
 ]
 
 
@@ -272,7 +308,7 @@ def test_c2_full_size_modal_property_two_iterations():
     ctx.close()
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
 def test_full_size_single_steps(cfg):
     """One coarse (tau = Delta T) and one fine (tau = delta t) step at the BASELINE size."""
     p = synth.CONFIGS[cfg]
