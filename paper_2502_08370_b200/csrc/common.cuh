@@ -160,6 +160,45 @@ __device__ __forceinline__ void seg_scan_bwd(double &Pm, double &Q, int W, int t
     }
 }
 
+// ---------------------------------------- cluster point-to-point (DSMEM + mbarrier) ---
+// A producer CTA writes 16 bytes straight into a consumer CTA's shared memory with st.async,
+// which signals the consumer's mbarrier (complete_tx) when the bytes land; the consumer arms
+// the barrier with the byte count it expects and waits on the phase parity.  No cluster-wide
+// barrier (and none of its release/acquire fences on outstanding global traffic) is needed.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(unsigned long long *mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *mb, unsigned parity) {
+    const unsigned a = smem_u32(mb);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+// st.async of a double2 into CTA `rank`'s copy of the local shared object `dst`, completing
+// tx bytes on that CTA's mbarrier `mb` (local address of the same object)
+__device__ __forceinline__ void st_async_remote(double2 *dst, unsigned long long *mb, unsigned rank, double2 v) {
+    unsigned rd, rm;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rd) : "r"(smem_u32(dst)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rm) : "r"(smem_u32(mb)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(rd),
+                 "d"(v.x), "d"(v.y), "r"(rm)
+                 : "memory");
+}
+
 // Walk dispatch: `full` must be uniform over the CTA (every chunk of every line has LCH
 // elements, or the predicated variant runs).
 template <class V>

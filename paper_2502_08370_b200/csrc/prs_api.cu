@@ -19,6 +19,11 @@
 #include "lpass.cuh"
 #include "setup.cuh"
 #include "xpass.cuh"
+#include "xpass3.cuh"
+#include "lpass3.cuh"
+
+#include <algorithm>
+#include <cstdlib>
 
 using namespace prs;
 
@@ -99,6 +104,8 @@ struct prs_ctx {
     long long k_launch[3] = {0, 0, 0};
     double k_ms[3] = {0, 0, 0}, k_bytes[3] = {0, 0, 0};
     ncclComm_t comm = nullptr;
+    int num_sms = 148;
+    bool force_v2 = false;  // PRS_XPASS=2: use the non-persistent x-pass (A/B measurements)
     std::string err;
 };
 
@@ -212,8 +219,60 @@ struct EpiArgs {
     double *traj = nullptr;
 };
 
+// persistent pipelined x-pass (xpass3.cuh) when the shape allows it
+static bool xpass3_ok(const prs_ctx *ctx, long long B) {
+    const int n = ctx->p.n;
+    if (ctx->force_v2) return false;
+    if (n < 16 || n > 4096 || (n & (n - 1)) != 0) return false;
+    const long long lines = B * (ctx->p.dim == 2 ? (long long)n : (long long)n * n);
+    const int lpg = 4096 / n;
+    if (lines % lpg != 0) return false;
+    if (ctx->p.coef_kind && n % lpg != 0) return false;
+    return true;
+}
+
+static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out, long long B,
+                         const TimeArgs &ta, bool prof) {
+    const int n = ctx->p.n, dim = ctx->p.dim;
+    X3Args a{};
+    a.in = in;
+    a.out = out;
+    a.vol = ctx->vol;
+    a.n = n;
+    a.P = n / LCH;
+    a.lines_per_state = (dim == 2) ? n : n * n;
+    a.ngroups = B * ctx->vol / 4096;
+    a.dim = dim;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.creact = ctx->creact;
+    a.src_amp = (double)dim * M_PI * M_PI + ctx->p.c - 1.0;
+    a.sinpi = ctx->sinpi;
+    a.ta = ta;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    a.invd = f.invdx;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    const int dr = (scheme == PRS_DR) ? 1 : 0;
+    const int coef = ctx->p.coef_kind;
+    const int src = ctx->p.source_kind;
+    const size_t shm = xpass3_smem_bytes(coef);
+    void (*kern)(X3Args) = nullptr;
+#define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass3_kernel<C, D, S_>;
+    XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
+#undef XK
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    const long long grid = std::min<long long>(ctx->num_sms, a.ngroups);
+    if (prof) TRY(prof_begin(ctx));
+    kern<<<(unsigned)grid, X3T, shm, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    if (prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * (16.0 + (coef ? 8.0 : 0.0))));
+    return PRS_OK;
+}
+
 static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
                         long long B, const TimeArgs &ta, bool prof) {
+    if (xpass3_ok(ctx, B)) return launch_xpass3(ctx, scheme, f, in, out, B, ta, prof);
     const int n = ctx->p.n, dim = ctx->p.dim;
     XArgs a{};
     a.in = in;
@@ -259,10 +318,85 @@ static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const dou
     return PRS_OK;
 }
 
+// persistent pipelined strided pass (lpass3.cuh): n = 16 * 2^k in [64, 4096]
+static int launch_lpass3(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out, long long B,
+                         const EpiArgs &ep, bool prof) {
+    const int n = ctx->p.n, dim = ctx->p.dim;
+    L3Args a{};
+    a.in = in;
+    a.out = out;
+    a.vol = ctx->vol;
+    a.n = n;
+    if (axis == 1) {
+        a.Sl = n;
+        a.nq = (dim == 2) ? 1 : n;
+        a.Sq = (long long)n * n;
+    } else {
+        a.Sl = (long long)n * n;
+        a.nq = n;
+        a.Sq = n;
+    }
+    a.CL = std::max(1, n / 512);
+    a.R = n / a.CL;
+    a.CP = a.R / LCH;
+    a.PW = L3T / a.CP;
+    a.nwb = n / a.PW;
+    a.npanels = B * a.nq * a.nwb;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    a.invd = f.invdy;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    a.e_gc = ep.gc;
+    a.e_gcache = ep.gcache;
+    a.e_delta = ep.delta;
+    a.e_traj = ep.traj;
+    a.e_red = ctx->red;
+    const int coef = ctx->p.coef_kind;
+    const size_t shm = lpass3_smem_bytes(a.PW, a.R, a.CL, coef);
+    void (*kern)(L3Args) = nullptr;
+#define LK(W, C, E) if (a.PW == W && coef == C && ep.kind == E) kern = lpass3_kernel<W, C, E>;
+#define LKW(W) LK(W, 0, 0) LK(W, 0, 1) LK(W, 0, 2) LK(W, 0, 3) LK(W, 1, 0) LK(W, 1, 1) LK(W, 1, 2) LK(W, 1, 3)
+    LKW(8) LKW(16) LKW(32) LKW(64)
+#undef LKW
+#undef LK
+    if (!kern) {
+        ctx->err = "lpass3: unsupported panel width";
+        return PRS_EUNSUPPORTED;
+    }
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    if (a.CL > 1) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const long long nclusters = std::min<long long>(std::max(1, ctx->num_sms / a.CL), a.npanels);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nclusters * a.CL));
+    cfg.blockDim = dim3(L3T);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (prof) TRY(prof_begin(ctx));
+    CK(cudaLaunchKernelEx(&cfg, kern, a));
+    TRY(last_launch(ctx));
+    if (prof) {
+        double per = 16.0 + (coef ? 8.0 : 0.0);
+        if (ep.kind == EPI_DELTA) per += 8.0;
+        TRY(prof_end(ctx, PRS_K_LPASS, (double)B * (double)ctx->vol * per));
+    }
+    return PRS_OK;
+}
+
 // strided pass along axis d (1 = y, 2 = z) over B states in place (in == out allowed)
 static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out,
                         long long B, const EpiArgs &ep, bool prof) {
     const int n = ctx->p.n, dim = ctx->p.dim;
+    if (!ctx->force_v2 && n >= 64 && n <= 4096 && (n & (n - 1)) == 0)
+        return launch_lpass3(ctx, axis, f, in, out, B, ep, prof);
     LArgs a{};
     a.in = in;
     a.out = out;
@@ -452,6 +586,11 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         }                                                                        \
     } while (0)
     CKC(cudaGetDevice(&ctx->device));
+    CKC(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    {
+        const char *xv = getenv("PRS_XPASS");
+        ctx->force_v2 = xv && xv[0] == '2';
+    }
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;
     } else {
