@@ -39,9 +39,21 @@ def parse():
     ap.add_argument("--impl", default="prs", choices=["prs", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
+                    help="override a Problem field of the workload (experiments; the default "
+                         "run uses the BASELINE config unchanged)")
     ap.add_argument("--profile-launches", action="store_true",
                     help="under ncu: only a short run, no timing extras")
     return ap.parse_args()
+
+
+def workload(args):
+    p = synth.CONFIGS[args.config]
+    for kv in args.set:
+        k, v = kv.split("=", 1)
+        cur = getattr(p, k)
+        p = p.replace(**{k: type(cur)(float(v)) if not isinstance(cur, str) else v})
+    return p
 
 
 def updates_per_step(p) -> int:
@@ -148,7 +160,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    p = synth.CONFIGS[args.config]
+    p = workload(args)
     reps = oracle_reps_for(p)
     for _ in range(args.warmup):
         oracle_sample(p, 1)
@@ -184,7 +196,7 @@ def run_prs(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    p = synth.CONFIGS[args.config]
+    p = workload(args)
     uid = None
     if world > 1:
         obj = [prs.nccl_unique_id() if rank == 0 else None]

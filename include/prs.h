@@ -62,7 +62,8 @@ typedef struct prs_problem {
  * tau in {Delta T, delta t}.  rank/nranks shard the N slices in contiguous
  * blocks (rank order = time order); nccl_uid is the 128-byte ncclUniqueId from
  * prs_nccl_unique_id() on rank 0, broadcast by the caller (NULL when nranks == 1).
- * cuda_stream is a cudaStream_t (NULL: the library creates one). */
+ * cuda_stream is a cudaStream_t (NULL: the library creates a blocking stream, ordered with
+ * the legacy default stream, so inputs written there are visible to the context's work). */
 int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_uid,
                void *cuda_stream, prs_ctx **out);
 

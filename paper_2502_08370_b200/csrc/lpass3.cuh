@@ -38,6 +38,7 @@ struct L3Args {
     const double *e_delta;
     double *e_traj;
     unsigned long long *e_red;
+    int noex;  // experiment switch: skip the cluster exchange (wrong results; timing only)
 };
 
 inline int lpass3_rows_stride(int R) { return R + R / LCH; }
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(L3T, 1) lpass3_kernel(L3Args a) {
         }
         cg::this_cluster().sync();  // barriers initialised before any remote complete_tx
     }
+    const bool ex = a.CL > 1 && !a.noex;
     const unsigned bytes_f = 16u * PW * crank, bytes_b = 16u * PW * (a.CL - 1 - crank);
     // panel p -> (state b, plane q, column block wb); nwb and nq are powers of two
     const int nwb_sh = __ffs(a.nwb) - 1, nq_sh = __ffs(a.nq) - 1;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(L3T, 1) lpass3_kernel(L3Args a) {
         const int it = iter;  // panel counter of this cluster
         const int par = (int)(it & 1);         // cluster totals double-buffered by parity
         const unsigned wpar = (unsigned)((it >> 1) & 1);
-        if (a.CL > 1 && tid == 0) {
+        if (ex && tid == 0) {
             if (crank > 0) mbar_arrive_expect(&mbf[par], bytes_f);
             if (crank < a.CL - 1) mbar_arrive_expect(&mbb[par], bytes_b);
         }
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(L3T, 1) lpass3_kernel(L3Args a) {
             YB = fma(s.x, YB, s.y);
             YA = s.x * YA;
         }
-        if (a.CL > 1) {
+        if (ex) {
             if (t == CP - 1) {  // push the CTA total of column w to every later CTA of the cluster
                 const double2 tot = make_double2(A * YA, fma(A, YB, B));
                 for (int q = crank + 1; q < a.CL; ++q)
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(L3T, 1) lpass3_kernel(L3Args a) {
             XQ = fma(s.x, XQ, s.y);
             XP = s.x * XP;
         }
-        if (a.CL > 1) {
+        if (ex) {
             if (t == 0) {  // push the backward total to every earlier CTA
                 const double2 tot = make_double2(Pb * XP, fma(Pb, XQ, Qb));
                 for (int q = 0; q < crank; ++q)

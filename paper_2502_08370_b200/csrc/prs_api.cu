@@ -21,6 +21,8 @@
 #include "xpass.cuh"
 #include "xpass3.cuh"
 #include "lpass3.cuh"
+#include "lpass4.cuh"
+#include "lpass5.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -106,6 +108,9 @@ struct prs_ctx {
     ncclComm_t comm = nullptr;
     int num_sms = 148;
     bool force_v2 = false;  // PRS_XPASS=2: use the non-persistent x-pass (A/B measurements)
+    bool force_l3 = false;  // PRS_LPASS=3: cluster pass lpass3 instead of lpass4 / lpass5
+    double *l5buf = nullptr;  // lpass5 block tuples and block y/x
+    size_t l5_bytes = 0;
     std::string err;
 };
 
@@ -354,9 +359,15 @@ static int launch_lpass3(prs_ctx *ctx, int axis, const TauFactors &f, const doub
     a.e_traj = ep.traj;
     a.e_red = ctx->red;
     const int coef = ctx->p.coef_kind;
-    const size_t shm = lpass3_smem_bytes(a.PW, a.R, a.CL, coef);
+    // clusters (long lines): one exchange of composed tuples per panel, hidden behind the
+    // previous panel (lpass4); single-CTA lines: lpass3
+    const bool use4 = a.CL > 1 && !ctx->force_l3;
+    a.noex = getenv("PRS_EXP_NOEX") ? 1 : 0;
+    const size_t shm = use4 ? lpass4_smem_bytes(a.PW, a.R, a.CL, coef) : lpass3_smem_bytes(a.PW, a.R, a.CL, coef);
     void (*kern)(L3Args) = nullptr;
-#define LK(W, C, E) if (a.PW == W && coef == C && ep.kind == E) kern = lpass3_kernel<W, C, E>;
+#define LK(W, C, E)                                                   \
+    if (a.PW == W && coef == C && ep.kind == E)                       \
+        kern = use4 ? lpass4_kernel<W, C, E> : lpass3_kernel<W, C, E>;
 #define LKW(W) LK(W, 0, 0) LK(W, 0, 1) LK(W, 0, 2) LK(W, 0, 3) LK(W, 1, 0) LK(W, 1, 1) LK(W, 1, 2) LK(W, 1, 3)
     LKW(8) LKW(16) LKW(32) LKW(64)
 #undef LKW
@@ -391,10 +402,76 @@ static int launch_lpass3(prs_ctx *ctx, int axis, const TauFactors &f, const doub
     return PRS_OK;
 }
 
+// long strided lines (n >= 2048): tuple / scan / finish over 64 x 64 tiles (lpass5.cuh)
+static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out, long long B,
+                         const EpiArgs &ep, bool prof) {
+    const int n = ctx->p.n, dim = ctx->p.dim;
+    L5Args a{};
+    a.in = in;
+    a.out = out;
+    a.vol = ctx->vol;
+    a.n = n;
+    if (axis == 1) {
+        a.Sl = n;
+        a.nq = (dim == 2) ? 1 : n;
+        a.Sq = (long long)n * n;
+    } else {
+        a.Sl = (long long)n * n;
+        a.nq = n;
+        a.Sq = n;
+    }
+    a.nrb = n / L5RB;
+    a.ncb = n / L5W;
+    a.ntiles = B * a.nq * a.nrb * a.ncb;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    a.invd = f.invdy;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    a.tstride = B * a.nq * a.nrb * (long long)n;
+    const size_t need = sizeof(double) * 7 * (size_t)a.tstride;
+    if (ctx->l5_bytes < need) {
+        if (ctx->l5buf) CK(cudaFree(ctx->l5buf));
+        ctx->l5buf = nullptr;
+        CK(cudaMalloc(&ctx->l5buf, need));
+        ctx->l5_bytes = need;
+    }
+    a.tt = ctx->l5buf;
+    a.yx = ctx->l5buf + 5 * a.tstride;
+    a.e_gc = ep.gc;
+    a.e_gcache = ep.gcache;
+    a.e_delta = ep.delta;
+    a.e_traj = ep.traj;
+    a.e_red = ctx->red;
+    const int coef = ctx->p.coef_kind;
+    void (*k1)(L5Args) = coef ? lp5_tuples_kernel<1> : lp5_tuples_kernel<0>;
+    void (*k3)(L5Args) = nullptr;
+#define LK(C, E) if (coef == C && ep.kind == E) k3 = lp5_finish_kernel<C, E>;
+    LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
+#undef LK
+    const long long ncols = B * a.nq * (long long)n;
+    if (prof) TRY(prof_begin(ctx));
+    k1<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    lp5_scan_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, ctx->stream>>>(a, ncols);
+    TRY(last_launch(ctx));
+    k3<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    if (prof) {
+        double per = 16.0 + (coef ? 8.0 : 0.0);
+        if (ep.kind == EPI_DELTA) per += 8.0;
+        TRY(prof_end(ctx, PRS_K_LPASS, (double)B * (double)ctx->vol * per));
+    }
+    return PRS_OK;
+}
+
 // strided pass along axis d (1 = y, 2 = z) over B states in place (in == out allowed)
 static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out,
                         long long B, const EpiArgs &ep, bool prof) {
     const int n = ctx->p.n, dim = ctx->p.dim;
+    if (!ctx->force_v2 && !ctx->force_l3 && n >= 2048 && n <= 4096 && (n & (n - 1)) == 0)
+        return launch_lpass5(ctx, axis, f, in, out, B, ep, prof);
     if (!ctx->force_v2 && n >= 64 && n <= 4096 && (n & (n - 1)) == 0)
         return launch_lpass3(ctx, axis, f, in, out, B, ep, prof);
     LArgs a{};
@@ -590,11 +667,15 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
     {
         const char *xv = getenv("PRS_XPASS");
         ctx->force_v2 = xv && xv[0] == '2';
+        const char *lv = getenv("PRS_LPASS");
+        ctx->force_l3 = lv && lv[0] == '3';
     }
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;
     } else {
-        CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        // a blocking stream: it orders with the legacy default stream, on which callers that
+        // pass no stream (e.g. PyTorch's default stream) fill the input buffers
+        CKC(cudaStreamCreate(&ctx->stream));
         ctx->own_stream = true;
     }
     const size_t sb = ctx->sbytes;
@@ -669,6 +750,7 @@ void prs_destroy(prs_ctx *ctx) {
     dd_free(ctx->dd);
     if (ctx->red) cudaFree(ctx->red);
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
+    if (ctx->l5buf) cudaFree(ctx->l5buf);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

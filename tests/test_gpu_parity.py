@@ -63,6 +63,11 @@ for n in (1, 2, 5, 16, 17, 31, 64, 100, 256, 257, 513, 1100):
     for coef in (0, 1):
         for src in (0, 1):
             STEP_CASES.append(Problem(dim=2, n=n, c=1.0, coef=coef, source=src, N=4, s=3))
+# power-of-two sizes take the persistent pipelined kernels; 1024 / 2048 exercise clusters of
+# 2 / 4 CTAs per strided line
+for n in (1024, 2048):
+    STEP_CASES.append(Problem(dim=2, n=n, c=1.0, coef=1, source=0, N=4, s=3))
+    STEP_CASES.append(Problem(dim=2, n=n, c=1.0, coef=0, source=1, N=4, s=3))
 for n in (1, 5, 17, 40):
     STEP_CASES.append(Problem(dim=3, n=n, c=1.0, source=1, N=4, s=3))
 
