@@ -236,7 +236,7 @@ def run_prs(args):
     torch.cuda.synchronize()
     launches = ctx.launches() - l0
     ms = ev0.elapsed_time(ev1)
-    stats = {k: ctx.kernel_stats(k) for k in (prs.PRS_K_XPASS, prs.PRS_K_LPASS)}
+    stats = {k: ctx.kernel_stats(k) for k in (prs.PRS_K_XPASS, prs.PRS_K_LPASS, prs.PRS_K_DD)}
     ctx.set_profiling(False)
     clk = clocks.stop()
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -272,21 +272,35 @@ def run_prs(args):
 
     # ---- roofline of the dominant kernel (live CUDA events around each launch) ----
     dom = max(stats, key=lambda k: stats[k][1])
-    nl, kms, kbytes = stats[dom]
-    peak, peak_src = measured_peaks()
-    achieved = (kbytes / nl) / ((kms / nl) / 1e3) / 1e9 if nl else 0.0
+    nl, kms, kwork = stats[dom]
     names = {prs.PRS_K_XPASS: "xpass_kernel (x-line solve + fused RHS)",
-             prs.PRS_K_LPASS: "lpass_kernel (strided y-line solve + epilogue)"}
+             prs.PRS_K_LPASS: "lpass_kernel (strided line solve + epilogue)",
+             prs.PRS_K_DD: "dd_stage_kernel (DD strip-block stage)"}
     tr = ncu_traffic(args.config)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    per_launch_s = (kms / nl) / 1e3 if nl else float("nan")
+    if dom == prs.PRS_K_DD:
+        # fp64 FMA pipe: 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (B200_PROFILING.md units)
+        peak, peak_src, unit, bound = 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 DFMA/clk x 1.965 GHz", "TFLOP/s", "alu"
+        achieved = (kwork / nl) / per_launch_s / 1e12 if nl else 0.0
+    else:
+        peak, peak_src = measured_peaks()
+        unit, bound = "GB/s", "hbm"
+        achieved = (kwork / nl) / per_launch_s / 1e9 if nl else 0.0
+
+    def rate(v):
+        if not v[0]:
+            return None
+        r = (v[2] / v[0]) / ((v[1] / v[0]) / 1e3)
+        return r / 1e12 if v is stats.get(prs.PRS_K_DD) else r / 1e9
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": (tr or {}).get(names[dom].split()[0]),
             "kernel": names[dom], "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": kbytes / nl if nl else None,
+            "algorithmic_work_per_launch": kwork / nl if nl else None,
             "avg_launch_ms": kms / nl if nl else None,
             "share_of_step": kms / ms if ms else None,
             "other_kernels": {names[k]: {"launches": v[0], "ms": v[1],
-                                         "GBps": (v[2] / v[0]) / ((v[1] / v[0]) / 1e3) / 1e9 if v[0] else None}
-                              for k, v in stats.items()}}
+                                         ("TFLOPs" if k == prs.PRS_K_DD else "GBps"): rate(v)}
+                              for k, v in stats.items() if v[0]}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sec, meta = oracle_sample(p, oracle_reps_for(p))

@@ -110,8 +110,9 @@ int prs_step_batch(prs_ctx *ctx, int which, int slice0, int j, const double *in,
  * every fine-sweep kernel launch is bracketed by CUDA events on the context stream and
  * prs_kernel_stats(kind) returns, for kind PRS_K_XPASS (contiguous-axis line solve),
  * PRS_K_LPASS (strided-axis line solve) or PRS_K_DD (DD strip-block stage), the launch
- * count, the summed device time (ms, synchronises) and the summed ALGORITHMIC bytes
- * (state read + state write + precomputed factors read). */
+ * count, the summed device time (ms, synchronises) and the summed ALGORITHMIC work: bytes
+ * (state read + state write + precomputed factors read) for the line passes,
+ * fp64 flops for PRS_K_DD (two W x W transforms + the y solve per support point). */
 #define PRS_K_XPASS 0
 #define PRS_K_LPASS 1
 #define PRS_K_DD 2

@@ -33,6 +33,7 @@
 #include "../../include/prs.h"
 #include "common.cuh"
 #include "lpass.cuh"
+#include "xpass3.cuh"
 
 struct prs_ctx;
 int prs_internal_prof_begin(prs_ctx *ctx);
@@ -41,9 +42,8 @@ int prs_internal_prof_end(prs_ctx *ctx, int kind, double bytes);
 namespace prs {
 
 constexpr int DD_RMAX = 128;   // rows per CTA
-constexpr int DD_WMAX = 152;   // widest block
-constexpr int DD_WPAD = 164;   // shared row stride of a tile (>= DD_WMAX, == 4 mod 16)
-constexpr int DD_CWMAX = 19;   // columns per GEMM thread, ceil(DD_WMAX / 8)
+constexpr int DD_WMAX = 144;   // widest block (16 column groups x 9)
+constexpr int DD_WPAD = 148;   // shared row stride of a tile (>= DD_WMAX, == 4 mod 16)
 constexpr int DD_KC = 16;      // Q rows staged per k-chunk
 constexpr int DD_THREADS = 256;
 
@@ -235,47 +235,78 @@ struct DDStageArgs {
 };
 
 // GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place.
-__device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
-    const int tid = threadIdx.x;
-    const int rg = tid >> 3, cg = tid & 7;
-    const int CW = (W + 7) >> 3;
-    double acc[4][DD_CWMAX];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int j = 0; j < DD_CWMAX; ++j) acc[r][j] = 0.0;
-    for (int k0 = 0; k0 < W; k0 += DD_KC) {
-        const int kc = min(DD_KC, W - k0);
-        __syncthreads();  // previous chunk consumed
-        for (int e = tid; e < kc * W; e += blockDim.x) Ms[(e / W) * DD_WPAD + (e % W)] = __ldg(M + (long long)k0 * W + e);
-        __syncthreads();
-        for (int kk = 0; kk < kc; ++kk) {
-            double f[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int l = rg + 32 * r;
-                f[r] = (l < nrow) ? T[cpad(l) * DD_WPAD + k0 + kk] : 0.0;
-            }
-            const double *mrow = Ms + kk * DD_WPAD + cg * CW;
-#pragma unroll
-            for (int j = 0; j < DD_CWMAX; ++j) {
-                if (j < CW) {
-                    const double m = mrow[j];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) acc[r][j] = fma(f[r], m, acc[r][j]);
-                }
-            }
+// 256 threads = 16 row groups x 16 column groups; each thread accumulates 8 rows (rg + 16 r)
+// x 9 columns (9 cg + j) in registers (72 fp64 FMAs per 17 shared loads per k).  M streams
+// through two shared k-chunks of DD_KC rows with cp.async (next chunk in flight while the
+// current one is consumed).  Columns >= W of T and of the staged M rows are zero, so the
+// inner loops need no predicates; rows >= nrow are computed and discarded.
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void dd_stage_mchunk(const double *M, int W, int k0, double *dst) {
+    const int kc = min(DD_KC, W - k0);
+    if ((W & 1) == 0) {  // 16-byte pieces (rows of M are 16-byte aligned)
+        const int pieces = kc * (W / 2);
+        for (int e = threadIdx.x; e < pieces; e += blockDim.x) {
+            const int r = e / (W / 2), h = e - r * (W / 2);
+            cp_async16(dst + r * DD_WPAD + 2 * h, M + (long long)(k0 + r) * W + 2 * h);
+        }
+    } else {
+        for (int e = threadIdx.x; e < kc * W; e += blockDim.x) {
+            const int r = e / W, c = e - r * W;
+            cp_async8(dst + r * DD_WPAD + c, M + (long long)(k0 + r) * W + c);
         }
     }
-    __syncthreads();  // all reads of T done before the in-place write
+}
+__device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
+    const int tid = threadIdx.x;
+    const int cg = tid & 15, rg = tid >> 4;
+    double acc[8][9];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int l = rg + 32 * r;
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int j = 0; j < 9; ++j) acc[r][j] = 0.0;
+    const int nk = (W + DD_KC - 1) / DD_KC;
+    __syncthreads();  // Ms aliases the y-solve scratch: all of its readers are done
+    // zero the staged chunks once (columns >= W stay zero; stale rows of a partial last chunk
+    // only ever meet the zero columns >= W of T)
+    for (int e = tid; e < 2 * DD_KC * DD_WPAD; e += blockDim.x) Ms[e] = 0.0;
+    __syncthreads();
+    dd_stage_mchunk(M, W, 0, Ms);
+    cp_async_commit();
+    for (int kb = 0; kb < nk; ++kb) {
+        double *cur = Ms + (kb & 1) * DD_KC * DD_WPAD;
+        if (kb + 1 < nk) dd_stage_mchunk(M, W, (kb + 1) * DD_KC, Ms + ((kb + 1) & 1) * DD_KC * DD_WPAD);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const int k0 = kb * DD_KC;
+        const double *trow = T + k0;
+        const double *mrow = cur + 9 * cg;
+#pragma unroll
+        for (int kk = 0; kk < DD_KC; ++kk) {
+            double f[8], m[9];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) f[r] = trow[cpad(rg + 16 * r) * DD_WPAD + kk];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) m[j] = mrow[kk * DD_WPAD + j];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int j = 0; j < 9; ++j) acc[r][j] = fma(f[r], m[j], acc[r][j]);
+        }
+        __syncthreads();  // chunk consumed before it is refilled
+    }
+    // all reads of T are done (last barrier above): write in place
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int l = rg + 16 * r;
         if (l < nrow) {
 #pragma unroll
-            for (int j = 0; j < DD_CWMAX; ++j) {
-                const int col = cg * CW + j;
-                if (j < CW && col < W) T[cpad(l) * DD_WPAD + col] = acc[r][j];
+            for (int j = 0; j < 9; ++j) {
+                const int col = 9 * cg + j;
+                if (col < W) T[cpad(l) * DD_WPAD + col] = acc[r][j];
             }
         }
     }
@@ -286,9 +317,9 @@ template <int DR, int SRC>
 __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     extern __shared__ double sh[];
     double *T = sh;                                          // (cpad(R-1)+1) x DD_WPAD
-    double *Ms = sh + (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // DD_KC x DD_WPAD
-    double2 *sc = reinterpret_cast<double2 *>(Ms + DD_KC * DD_WPAD);  // 8 x DD_WMAX chunk maps
-    double2 *ctf = sc + 8 * DD_WMAX;                          // cluster totals fwd
+    double *Ms = sh + (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // 2 x DD_KC x DD_WPAD (GEMM)
+    double2 *sc = reinterpret_cast<double2 *>(Ms);           // 8 x DD_WMAX chunk maps (y solve)
+    double2 *ctf = reinterpret_cast<double2 *>(Ms + 2 * DD_KC * DD_WPAD);  // cluster totals fwd
     double2 *ctb = ctf + DD_WMAX;                             // cluster totals bwd
     __shared__ double sdmax;
     __shared__ unsigned long long sbad;
@@ -341,6 +372,11 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
             }
         }
         T[cpad(rl) * DD_WPAD + ci] = r;
+    }
+    // zero the columns W..DD_WMAX-1 the unpredicated GEMM reads
+    for (int e = tid; e < nrow * (DD_WMAX - W); e += blockDim.x) {
+        const int rl = e / (DD_WMAX - W), ci = W + e % (DD_WMAX - W);
+        T[cpad(rl) * DD_WPAD + ci] = 0.0;
     }
     // ---- G = F Q ----
     dd_tile_gemm(T, a.Q[blk], W, nrow, Ms);
@@ -555,8 +591,10 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
 }
 
 inline size_t dd_stage_smem_bytes() {
-    return sizeof(double) * ((size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD + DD_KC * DD_WPAD) +
-           sizeof(double2) * (8 * DD_WMAX + 2 * DD_WMAX);
+    // tile + two staged M chunks (the y-solve chunk maps alias them) + cluster totals
+    static_assert(2 * DD_KC * DD_WPAD * sizeof(double) >= 8 * DD_WMAX * sizeof(double2), "sc alias");
+    return sizeof(double) * ((size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD + 2 * DD_KC * DD_WPAD) +
+           sizeof(double2) * (2 * DD_WMAX);
 }
 
 // ------------------------------------------------------------------ host side ------
@@ -777,10 +815,11 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
             return PRS_ECUDA;
         }
         if (prof) {
-            long long cols = 0;
-            for (int w : d.bW[stage]) cols += w;
-            // algorithmic bytes: read + write of the block's support points
-            if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * cols * n * 16.0) != PRS_OK) return PRS_ECUDA;
+            // algorithmic fp64 flops: per support point of a W-wide block, two W x W
+            // transforms (2 W each) and the tridiagonal solve along y (~10)
+            double flops = 0.0;
+            for (int w : d.bW[stage]) flops += (double)w * n * (4.0 * w + 10.0);
+            if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
         }
     }
     return PRS_OK;

@@ -132,17 +132,19 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
     struct LineScalars {
         double kfm, kfp, hsx, srcf;
     };
+    // (raw loads only: the 0.5 factors are applied at the use, one group later, so no
+    // instruction waits on these loads here)
     auto line_scalars = [&](long long gg) {
-        LineScalars s{0.5, 0.5, 0.0, 0.0};
+        LineScalars s{1.0, 1.0, 0.0, 0.0};
         if (gg >= G) return s;
         const long long gl = gg * lpg + l;
         const long long bs = gl >> lps_sh;
         const int jj = (int)(gl & (a.lines_per_state - 1));
         if (DR && COEF) {
-            s.kfm = 0.5 * __ldg(a.s2f + jj);
-            s.kfp = 0.5 * __ldg(a.s2f + jj + 1);
+            s.kfm = __ldg(a.s2f + jj);
+            s.kfp = __ldg(a.s2f + jj + 1);
         }
-        if (COEF) s.hsx = 0.5 * __ldg(a.s2n + ((a.dim == 2) ? jj : jj % n));
+        if (COEF) s.hsx = __ldg(a.s2n + ((a.dim == 2) ? jj : jj % n));
         if (SRC) {
             const double ampt = a.src_amp * exp(-src_time(a.ta, bs));
             const double sj =
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
             const bool hm = j > 0, hp = j < n - 1;
             const double *um = (l > 0) ? U + (k - P) * X3C : ub(g - 1) + (k - P + X3T) * X3C;
             const double *up = (l < lpg - 1) ? U + (k + P) * X3C : ub(g + 1) + (k + P - X3T) * X3C;
-            const double kfm = cur.kfm, kfp = cur.kfp;
+            const double kfm = 0.5 * cur.kfm, kfp = 0.5 * cur.kfp;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const double2 xm = hm ? *reinterpret_cast<const double2 *>(um + 2 * u) : make_double2(0.0, 0.0);
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
                 idr[2 * u + 1] = x.y;
             }
             idm1 = (t > 0) ? I[-X3C + LCH - 1] : 0.0;
-            hsx = cur.hsx;
+            hsx = 0.5 * cur.hsx;
         }
         auto af = [&](int i) { return -tauh * fma(hsx, sf[i], 1.0); };
         auto cm = [&](int i) { return COEF ? af(i) * (i == 0 ? idm1 : idr[i - 1]) : tm[i]; };
