@@ -33,6 +33,9 @@ struct L5Args {
     int nq;               // planes per state
     int nrb, ncb;         // row blocks, column blocks per plane
     long long ntiles;     // batch * nq * nrb * ncb
+    long long nsq;        // batch * nq
+    int order;            // tile order: 0 column block fastest; 1 state fastest (pivot tiles
+                          // shared by all states are then read by co-resident CTAs: L2 hits)
     double tau, h2inv;
     CoefTab tab;
     const double *invd, *s2n, *s2f;
@@ -80,10 +83,17 @@ struct L5Tile {
 };
 __device__ __forceinline__ L5Tile l5_tile(const L5Args &a, long long tile) {
     L5Tile T;
-    T.cb = (int)(tile % a.ncb);
-    long long r = tile / a.ncb;
-    T.rb = (int)(r % a.nrb);
-    T.sq = r / a.nrb;
+    if (a.order) {
+        T.sq = tile % a.nsq;
+        const long long r = tile / a.nsq;
+        T.cb = (int)(r % a.ncb);
+        T.rb = (int)(r / a.ncb);
+    } else {
+        T.cb = (int)(tile % a.ncb);
+        const long long r = tile / a.ncb;
+        T.rb = (int)(r % a.nrb);
+        T.sq = r / a.nrb;
+    }
     const long long b = T.sq / a.nq;
     const int q = (int)(T.sq - b * a.nq);
     T.base = b * a.vol + (long long)q * a.Sq;
@@ -165,6 +175,31 @@ __global__ void lp5_scan_kernel(L5Args a, long long ncols) {
         a.yx[a.tstride + o] = X;
         // x at the first row of block rb, from its tuple and its incoming y
         X = fma(a.tt[2 * a.tstride + o], X, fma(a.tt[4 * a.tstride + o], a.yx[o], a.tt[3 * a.tstride + o]));
+    }
+}
+
+// Same scan when the block tuples come from xpass6: data parts B (tt[1]) and Q (tt[3]) per
+// state, pivot-only parts A, P, R from the per-tau table apr = [3][nrb][n].
+__global__ void lp6_scan_kernel(L5Args a, const double *__restrict__ apr, long long ncols) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= ncols) return;
+    const long long sq = idx / a.n;
+    const int col = (int)(idx - sq * a.n);
+    const long long o0 = sq * a.nrb * a.n + col;
+    const long long plane = (long long)a.nrb * a.n;
+    const double *tB = a.tt + a.tstride, *tQ = a.tt + 3 * a.tstride;
+    double Y = 0.0;
+    for (int rb = 0; rb < a.nrb; ++rb) {
+        const long long o = o0 + (long long)rb * a.n;
+        a.yx[o] = Y;
+        Y = fma(__ldg(apr + (long long)rb * a.n + col), Y, tB[o]);
+    }
+    double X = 0.0;
+    for (int rb = a.nrb - 1; rb >= 0; --rb) {
+        const long long o = o0 + (long long)rb * a.n;
+        const long long to = (long long)rb * a.n + col;
+        a.yx[a.tstride + o] = X;
+        X = fma(__ldg(apr + plane + to), X, fma(__ldg(apr + 2 * plane + to), a.yx[o], tQ[o]));
     }
 }
 

@@ -131,6 +131,47 @@ def test_batched_step_parity(p):
     ctx.close()
 
 
+# 2-D lines of 1024 / 2048 / 4096: the default long-line path and the opt-in xpass6 paths
+# (x solve + y block tuples, lp6_scan, lp5_finish over slice-fastest tiles, padded slices);
+# B states of different magnitude so a mix-up between states cannot pass
+FUSED_CASES = [
+    Problem(dim=2, n=1024, c=1.0, coef=1, N=6, s=5, G=FIE, F=DR, source=0, init="modes", seed=3),
+    Problem(dim=2, n=1024, c=1.0, coef=0, N=6, s=5, G=DR, F=FIE, source=1),
+    Problem(dim=2, n=1024, c=2.0, coef=1, N=6, s=5, G=DR, F=FIE, source=1, init="modes", seed=6),
+    Problem(dim=2, n=2048, c=1.0, coef=1, N=4, s=3, G=DR, F=DR, source=0, init="modes", seed=4),
+]
+
+
+@pytest.mark.parametrize("mode", ["default", "1", "2"])
+@pytest.mark.parametrize("p", FUSED_CASES, ids=lambda p: p.label())
+def test_fused_long_line_batched_parity(p, mode, monkeypatch):
+    """mode: the default long-line path (xpass3 + lpass5), PRS_FUSED=1 (xpass6 with the y
+    block tuples fused) or 2 (xpass6 + lp5 tuple kernel); the library reads it at create."""
+    if mode != "default":
+        monkeypatch.setenv("PRS_FUSED", mode)
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    o = oracle.Oracle(p)
+    B = 5 if p.n <= 1024 else 3
+    base = synth.initial_state(p)
+    us = np.stack([base * (1.0 + 0.25 * b) + 1e-3 * rand_field(p, 40 + b) for b in range(B)])
+    du = dev(us)
+    out = torch.empty_like(du)
+    dt = p.T / (p.N * p.s)
+    dT = p.T / p.N
+    for which, j in ((1, 0), (1, 2), (0, 0)):
+        ctx.step_batch(which, 1, j, du, out, B)
+        got = host(out)
+        for b in range(B):
+            sch, tau = (p.F, dt) if which == 1 else (p.G, dT)
+            tn = float((1 + b) * p.s + j + 1) * dt if which == 1 else float(1 + b + 1) * dT
+            want = o.step(sch, tau, tn, us[b])
+            scales = (want, us[b], tau * o.apply(-1, us[b])) if sch == DR else (want, us[b])
+            e = nerr(got[b], want, *scales)
+            assert e <= TOL, (which, b, e)
+    ctx.close()
+
+
 # ----------------------------------------------------------- DD stage solves
 DD_STEP_CASES = [
     Problem(dim=2, n=32, c=1.0, split=1, dd_strips=4, dd_overlap=4, dd_ramp=0, N=4, s=3),
@@ -188,6 +229,8 @@ PARAREAL_CASES = [
     Problem(dim=2, n=48, c=1.0, N=8, s=8, G=DR, F=DR, init="modes", seed=0),        # c1 recipe
     Problem(dim=2, n=80, c=1.0, coef=1, N=6, s=8, G=FIE, F=DR, init="modes", seed=1),  # c3 recipe
     Problem(dim=2, n=80, c=1.0, coef=1, N=6, s=8, G=DR, F=DR, init="modes", seed=2),
+    # the fused long-line path end to end (every epilogue: INIT, DELTA, CORRECT)
+    Problem(dim=2, n=1024, c=1.0, coef=1, N=3, s=2, G=FIE, F=DR, init="modes", seed=1),
     Problem(dim=3, n=20, c=1.0, source=1, N=5, s=4, G=FIE, F=FIE),                  # c2 recipe
     Problem(dim=2, n=37, c=1.0, source=1, N=5, s=3, G=DR, F=FIE),
     Problem(dim=2, n=37, c=1.0, source=1, N=5, s=3, G=FIE, F=DR),
@@ -201,6 +244,16 @@ PARAREAL_CASES = [
 
 @pytest.mark.parametrize("p", PARAREAL_CASES, ids=lambda p: p.label())
 def test_parareal_iterates_match_oracle_every_iteration(p):
+    _parareal_vs_oracle(p)
+
+
+def test_parareal_fused_long_line_path(monkeypatch):
+    """The opt-in xpass6 path end to end (INIT, DELTA and CORRECT epilogues, padded slices)."""
+    monkeypatch.setenv("PRS_FUSED", "1")
+    _parareal_vs_oracle(Problem(dim=2, n=1024, c=1.0, coef=1, N=3, s=2, G=FIE, F=DR, init="modes", seed=1))
+
+
+def _parareal_vs_oracle(p):
     """A13: every iterate U^k_n, k = 0..N, and the update norms."""
     u0 = synth.initial_state(p)
     o = oracle.Oracle(p)
