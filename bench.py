@@ -44,6 +44,8 @@ def parse():
                          "run uses the BASELINE config unchanged)")
     ap.add_argument("--profile-launches", action="store_true",
                     help="under ncu: only a short run, no timing extras")
+    ap.add_argument("--no-time-to-tol", action="store_true",
+                    help="skip the parareal time-to-tolerance run and the sequential fine solve")
     return ap.parse_args()
 
 
@@ -54,6 +56,11 @@ def workload(args):
         cur = getattr(p, k)
         p = p.replace(**{k: type(cur)(float(v)) if not isinstance(cur, str) else v})
     return p
+
+
+def stop_tol(name: str) -> float:
+    """A7 / DESIGN.md R7-R8: c0 runs its fixed K = 8 (= N) iterations; c1-c4 stop at 1e-10."""
+    return 0.0 if name == "c0" else 1e-10
 
 
 def updates_per_step(p) -> int:
@@ -270,6 +277,38 @@ def run_prs(args):
                "d2h_bytes_per_step": (int(u0.nbytes) + 16) * world,
                "includes": "set_initial(host) + coarse_sweep + fine_sweep + correct + get_slice(host)"}
 
+    # ---- parareal time to tolerance (the metric's second part) and the sequential fine solve
+    # it competes with (same kernels, N s steps on one state, one GPU: SURVEY.md 8(d)) ----
+    ttt = None
+    if not args.no_time_to_tol:
+        tol = stop_tol(args.config)
+        barrier()
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        ctx.set_initial(u0_dev)
+        ctx.coarse_sweep()
+        k, hist = ctx.iterate(p.N, tol)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3, time.perf_counter() - t0], dtype=torch.float64,
+                          device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        seq = None
+        if rank == 0:
+            out_dev = torch.empty_like(u0_dev)
+            torch.cuda.synchronize()
+            s0 = time.perf_counter()
+            ctx.fine_solve(u0_dev, out_dev)
+            seq = time.perf_counter() - s0
+        barrier()
+        ttt = {"tol": tol, "stop": "max|U^{k+1}-U^k| / ||U_0||_inf <= tol or k = N (DESIGN.md R7)",
+               "iterations": k, "N": p.N, "time_to_tol_s": float(tt[0].item()),
+               "wall_s": float(tt[1].item()), "updates_last": hist[-1] if hist else None,
+               "sequential_fine_s": seq,
+               "speedup_vs_sequential_fine": (seq / float(tt[0].item())) if seq else None,
+               "sequential_fine": "prs_fine_solve: N s fine steps of one state on rank 0's GPU"}
+
     # ---- roofline of the dominant kernel (live CUDA events around each launch) ----
     dom = max(stats, key=lambda k: stats[k][1])
     nl, kms, kwork = stats[dom]
@@ -314,7 +353,7 @@ def run_prs(args):
                 "data": "synthetic", "config": workload_config(p, args.config, world),
                 "parallelism": f"time-slices x{world}",
                 "updates": upds, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-                "cpu_baseline": cpu, "e2e": e2e}
+                "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -106,6 +106,16 @@ int prs_step(prs_ctx *ctx, int scheme, double tau, double t_next, const double *
  * prs_fine_sweep.  Test hook for full-size batched parity. */
 int prs_step_batch(prs_ctx *ctx, int which, int slice0, int j, const double *in, double *out, int B);
 
+/* The sequential fine solution (PAPER.md:206-208 with every slice propagated by F in turn):
+ * nslices * s fine steps of size delta t from U_0 = u0 (n^dim doubles, host or device), the
+ * end state U(nslices Delta T) written to out (host or device).  Runs on the calling rank
+ * alone (no communication) in the fine-sweep kernels with batch 1; it is the baseline that
+ * parareal's time-to-tolerance is compared against, and finite termination's reference
+ * (PAPER.md:214).  Uses the fine-sweep work buffers: a fine sweep whose correction is still
+ * pending is invalidated (run prs_fine_sweep again).  Synchronises. */
+int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices, double *out,
+                   int out_on_device);
+
 /* Counters.  prs_launches: kernels this context has launched so far.  With profiling on,
  * every fine-sweep kernel launch is bracketed by CUDA events on the context stream and
  * prs_kernel_stats(kind) returns, for kind PRS_K_XPASS (contiguous-axis line solve),

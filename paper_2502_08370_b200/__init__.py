@@ -20,7 +20,7 @@ PRS_FIE, PRS_DR = 0, 1
 PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
 EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
-           "prs_get_slice", "prs_step", "prs_step_batch", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
+           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
            "prs_last_error", "prs_destroy"]
 
 
@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
             "prs_get_slice": ([V, I, V, I], I),
             "prs_step": ([V, I, D, D, V, V], I),
             "prs_step_batch": ([V, I, I, I, V, V, I], I),
+            "prs_fine_solve": ([V, V, I, I, V, I], I),
             "prs_set_profiling": ([V, I], I),
             "prs_launches": ([V], ctypes.c_longlong),
             "prs_kernel_stats": ([V, I, PL, PD, PD], I),
@@ -178,6 +179,14 @@ class Context:
         pi, _ = self._ptr(inp)
         po, _ = self._ptr(out)
         self._check(self.L.prs_step_batch(self.h, which, slice0, j, pi, po, B))
+        return out
+
+    def fine_solve(self, u0, out, nslices: int | None = None):
+        """Sequential fine solution: nslices * s fine steps from u0 (default: all N slices)."""
+        pi, di = self._ptr(u0)
+        po, do = self._ptr(out)
+        ns = self.prob.N if nslices is None else nslices
+        self._check(self.L.prs_fine_solve(self.h, pi, int(di), ns, po, int(do)))
         return out
 
     def set_profiling(self, on: bool):

@@ -1112,6 +1112,33 @@ int prs_step_batch(prs_ctx *ctx, int which, int slice0, int j, const double *in,
     return PRS_OK;
 }
 
+int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices, double *out, int out_on_device) {
+    if (!ctx || !u0 || !out || nslices < 0 || nslices > ctx->p.N) return PRS_EINVAL;
+    TRY(ensure_factors(ctx, 1, ctx->dt));
+    double *buf[2] = {ctx->fa, ctx->fb};  // the fine-sweep work buffers (slot 0 of each)
+    ctx->delta = nullptr;                 // a pending fine sweep is invalidated
+    CK(cudaMemcpyAsync(buf[0], u0, ctx->sbytes, u0_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream));
+    int cur = 0;
+    const int s = ctx->p.s;
+    for (int n = 0; n < nslices; ++n) {
+        for (int j = 0; j < s; ++j) {
+            TimeArgs ta;
+            ta.slice0 = n;
+            ta.tmul = s;
+            ta.toff = j + 1;
+            ta.tstep = ctx->dt;
+            EpiArgs ep;
+            TRY(run_step(ctx, ctx->p.F, ctx->fac[1], buf[cur], buf[cur ^ 1], 1, ta, ep, false, ctx->ss));
+            cur ^= 1;
+        }
+    }
+    CK(cudaMemcpyAsync(out, buf[cur], ctx->sbytes, out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PRS_OK;
+}
+
 int prs_set_profiling(prs_ctx *ctx, int on) {
     if (!ctx) return PRS_EINVAL;
     ctx->prof = on != 0;

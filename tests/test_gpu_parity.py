@@ -422,3 +422,27 @@ def test_c1_full_size_first_iterations():
     for k in range(2):
         scale = max(float(np.max(np.abs(u0))), float(np.max(np.abs(ctrajs[k]))))
         assert float(np.max(np.abs(gtrajs[k] - ctrajs[k]))) / scale <= TOL, k
+
+
+@pytest.mark.parametrize("p", [synth.CONFIGS["c0"],
+                               Problem(dim=2, n=48, c=1.0, coef=1, N=6, s=5, G=FIE, F=DR, init="modes", seed=7),
+                               Problem(dim=3, n=20, c=1.0, source=1, N=4, s=3),
+                               Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=4,
+                                       s=3, G=FIE, F=DR)],
+                         ids=lambda p: p.label())
+def test_fine_solve_matches_sequential_fine_solution(p):
+    """prs_fine_solve (the sequential baseline of time-to-tol) = the oracle's F^s chain."""
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    u0 = synth.initial_state(p)
+    want = oracle.Oracle(p).fine_solution(u0)
+    scale = max(float(np.max(np.abs(t))) for t in want)
+    out = torch.empty((p.n,) * p.dim, dtype=torch.float64, device="cuda")
+    for ns in (1, p.N // 2, p.N):
+        ctx.fine_solve(dev(u0), out, ns)
+        assert float(np.max(np.abs(host(out) - want[ns]))) / scale <= TOL, ns
+    # host buffers in and out
+    hout = np.empty((p.n,) * p.dim)
+    ctx.fine_solve(np.ascontiguousarray(u0), hout, p.N)
+    assert float(np.max(np.abs(hout - want[p.N]))) / scale <= TOL
+    ctx.close()
