@@ -345,38 +345,65 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     double ampt = 0.0;
     if (SRC) ampt = a.src_amp * exp(-src_time(a.ta, b));
 
-    // ---- load the right-hand side tile ----
-    for (int e = tid; e < nrow * W; e += blockDim.x) {
-        const int rl = e / W, ci = e % W;
-        const int l = r0 + rl, i = i0 + ci;
-        const long long g = (long long)l * n + i;
-        double r;
-        if (me == 0) {
-            const double u = Ub[g];
-            r = u;
-            if (SRC) r += a.tau * (ampt * a.sinpi[i] * a.sinpi[l]);
-            if (DR) {  // w = tau A_1 U (colour-1 operator) at (i, l)
-                const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
-                const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
-                const double rnode = rn_ot[i];
-                const double w = a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) +
-                                           rnode * (vp - 2.0 * u + vm)) * a.h2inv - rnode * a.c * u);
-                r += w;
+    // ---- load the right-hand side tile: one row per warp, columns across lanes; every
+    // global load of a row is issued before the first use (several rows' worth in flight) ----
+    constexpr int NCW = (DD_WMAX + 31) / 32;  // column slots per lane
+    {
+        const int wp = tid >> 5, ln = tid & 31;
+        for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
+            const int l = r0 + rl;
+            const long long g0 = (long long)l * n + i0;
+            double r[NCW], u[NCW];
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) {
+                const int ci = ln + 32 * k;
+                const bool in = ci < W;
+                const long long g = g0 + ci;
+                if (me == 0) {
+                    u[k] = in ? Ub[g] : 0.0;
+                    r[k] = 0.0;
+                } else {
+                    const bool done0 = in && rn_ot[i0 + ci] > 0.0;  // final after stage 0
+                    r[k] = done0 ? Vb[g] : 0.0;
+                    u[k] = (in && !done0) ? Ub[g] : 0.0;
+                }
             }
-        } else {
-            if (rn_ot[i] > 0.0) {
-                r = Vb[g];
-            } else {
-                r = Ub[g];
-                if (SRC) r += a.tau * (ampt * a.sinpi[i] * a.sinpi[l]);
+            double wv[NCW];
+            if (DR && me == 0) {  // w = tau A_1 U (colour-1 operator)
+#pragma unroll
+                for (int k = 0; k < NCW; ++k) {
+                    const int ci = ln + 32 * k, i = i0 + ci;
+                    wv[k] = 0.0;
+                    if (ci < W) {
+                        const long long g = g0 + ci;
+                        const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
+                        const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
+                        const double uu = u[k], rnode = rn_ot[i];
+                        wv[k] = a.tau * ((rf_ot[i + 1] * (up - uu) - rf_ot[i] * (uu - um) +
+                                          rnode * (vp - 2.0 * uu + vm)) * a.h2inv - rnode * a.c * uu);
+                    }
+                }
+            }
+            const double sl = SRC ? a.tau * ampt * a.sinpi[l] : 0.0;
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) {
+                const int ci = ln + 32 * k, i = i0 + ci;
+                double v = 0.0;  // columns W..DD_WMAX-1 are zero for the unpredicated GEMM
+                if (ci < W) {
+                    if (me == 0) {
+                        v = u[k];
+                        if (SRC) v += sl * a.sinpi[i];
+                        if (DR) v += wv[k];
+                    } else if (rn_ot[i] > 0.0) {
+                        v = r[k];
+                    } else {
+                        v = u[k];
+                        if (SRC) v += sl * a.sinpi[i];
+                    }
+                }
+                if (ci < DD_WMAX) T[cpad(rl) * DD_WPAD + ci] = v;
             }
         }
-        T[cpad(rl) * DD_WPAD + ci] = r;
-    }
-    // zero the columns W..DD_WMAX-1 the unpredicated GEMM reads
-    for (int e = tid; e < nrow * (DD_WMAX - W); e += blockDim.x) {
-        const int rl = e / (DD_WMAX - W), ci = W + e % (DD_WMAX - W);
-        T[cpad(rl) * DD_WPAD + ci] = 0.0;
     }
     // ---- G = F Q ----
     dd_tile_gemm(T, a.Q[blk], W, nrow, Ms);
@@ -539,39 +566,48 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     // ---- U = V Q^T ----
     dd_tile_gemm(T, a.QT[blk], W, nrow, Ms);
 
-    // ---- store (+ fused parareal epilogue for final values) ----
+    // ---- store (+ fused parareal epilogue for final values): one row per warp ----
     double dmax = 0.0;
     unsigned long long bad = 0;
-    for (int e = tid; e < nrow * W; e += blockDim.x) {
-        const int rl = e / W, ci = e % W;
-        const int l = r0 + rl, i = i0 + ci;
-        const long long g = (long long)l * n + i;
-        double x = T[cpad(rl) * DD_WPAD + ci];
-        if (DR && me == 0) {  // V = x - w
-            const double u = Ub[g];
-            const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
-            const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
-            const double rnode = rn_ot[i];
-            x -= a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) + rnode * (vp - 2.0 * u + vm)) * a.h2inv -
-                          rnode * a.c * u);
-        }
-        const bool final_here = (me == 1) || !(rn_ot[i] > 0.0);
-        const int ep = final_here ? a.epi : EPI_STORE;
-        const long long gb = b * a.vol + g;
-        if (ep == EPI_STORE) {
-            Vb[g] = x;
-        } else if (ep == EPI_DELTA) {
-            Vb[g] = x - a.e_gc[gb];
-        } else if (ep == EPI_CORRECT) {
-            const double nv = x + a.e_delta[g];
-            const double ov = a.e_traj[g];
-            a.e_gcache[g] = x;
-            a.e_traj[g] = nv;
-            dmax = fmax(dmax, fabs(nv - ov));
-            if (!isfinite(nv)) bad = 1;
-        } else {  // INIT
-            a.e_gcache[g] = x;
-            a.e_traj[g] = x;
+    {
+        const int wp = tid >> 5;
+        for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
+            const int l = r0 + rl;
+            const long long g0 = (long long)l * n + i0;
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) {
+                const int ci = lane + 32 * k, i = i0 + ci;
+                if (ci >= W) continue;
+                const long long g = g0 + ci;
+                double x = T[cpad(rl) * DD_WPAD + ci];
+                if (DR && me == 0) {  // V = x - w
+                    const double u = Ub[g];
+                    const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
+                    const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
+                    const double rnode = rn_ot[i];
+                    x -= a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) + rnode * (vp - 2.0 * u + vm)) *
+                                      a.h2inv -
+                                  rnode * a.c * u);
+                }
+                const bool final_here = (me == 1) || !(rn_ot[i] > 0.0);
+                const int ep = final_here ? a.epi : EPI_STORE;
+                const long long gb = b * a.vol + g;
+                if (ep == EPI_STORE) {
+                    Vb[g] = x;
+                } else if (ep == EPI_DELTA) {
+                    Vb[g] = x - a.e_gc[gb];
+                } else if (ep == EPI_CORRECT) {
+                    const double nv = x + a.e_delta[g];
+                    const double ov = a.e_traj[g];
+                    a.e_gcache[g] = x;
+                    a.e_traj[g] = nv;
+                    dmax = fmax(dmax, fabs(nv - ov));
+                    if (!isfinite(nv)) bad = 1;
+                } else {  // INIT
+                    a.e_gcache[g] = x;
+                    a.e_traj[g] = x;
+                }
+            }
         }
     }
     if (a.epi == EPI_CORRECT) {
