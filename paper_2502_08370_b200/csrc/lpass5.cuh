@@ -36,6 +36,7 @@ struct L5Args {
     long long nsq;        // batch * nq
     int order;            // tile order: 0 column block fastest; 1 state fastest (pivot tiles
                           // shared by all states are then read by co-resident CTAs: L2 hits)
+    int s8, nsg8;         // lpass8: slices per CTA, slice groups
     double tau, h2inv;
     CoefTab tab;
     const double *invd, *s2n, *s2f;

@@ -24,6 +24,7 @@
 #include "lpass4.cuh"
 #include "lpass5.cuh"
 #include "xpass6.cuh"
+#include "lpass8.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -116,6 +117,7 @@ struct prs_ctx {
     bool force_l3 = false;  // PRS_LPASS=3: cluster pass lpass3 instead of lpass4 / lpass5
     bool no_fused = false;  // PRS_FUSED=0: 2-D long lines take xpass3 + lpass5 (A/B measurements)
     bool fused_notup = false;  // PRS_FUSED=2: xpass6 without the fused y tuples + lp5 tuple kernel
+    bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
     double *l5buf = nullptr;  // lpass5 block tuples and block y/x
     size_t l5_bytes = 0;
     std::string err;
@@ -483,13 +485,37 @@ static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const doub
     LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
 #undef LK
     const long long ncols = B * a.nq * (long long)n;
+    const bool use8 = !ctx->no_l8 && a.nq == 1;
     if (prof) TRY(prof_begin(ctx));
-    k1<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
-    TRY(last_launch(ctx));
-    lp5_scan_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, ctx->stream>>>(a, ncols);
-    TRY(last_launch(ctx));
-    k3<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
-    TRY(last_launch(ctx));
+    if (use8) {
+        // persistent over slice groups: coefficients once per tile position, state tiles
+        // through a cp.async ring
+        a.nsq = B;
+        a.s8 = (int)std::min<long long>(B, 16);
+        a.nsg8 = (int)((B + a.s8 - 1) / a.s8);
+        const long long grid = (long long)a.nrb * a.ncb * a.nsg8;
+        const size_t shm = lpass8_smem_bytes();
+        void (*t8)(L5Args) = coef ? lp8_kernel<1, 0, 0> : lp8_kernel<0, 0, 0>;
+        void (*f8)(L5Args) = nullptr;
+#define LK(C, E) if (coef == C && ep.kind == E) f8 = lp8_kernel<C, E, 1>;
+        LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
+#undef LK
+        CK(cudaFuncSetAttribute(t8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        t8<<<(unsigned)grid, L5T, shm, ctx->stream>>>(a);
+        TRY(last_launch(ctx));
+        lp5_scan_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, ctx->stream>>>(a, ncols);
+        TRY(last_launch(ctx));
+        f8<<<(unsigned)grid, L5T, shm, ctx->stream>>>(a);
+        TRY(last_launch(ctx));
+    } else {
+        k1<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
+        TRY(last_launch(ctx));
+        lp5_scan_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, ctx->stream>>>(a, ncols);
+        TRY(last_launch(ctx));
+        k3<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
+        TRY(last_launch(ctx));
+    }
     if (prof) {
         double per = 16.0 + (coef ? 8.0 : 0.0);
         if (ep.kind == EPI_DELTA) per += 8.0;
@@ -838,6 +864,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         const char *fv = getenv("PRS_FUSED");
         ctx->no_fused = !(fv && (fv[0] == '1' || fv[0] == '2'));
         ctx->fused_notup = fv && fv[0] == '2';
+        const char *l8 = getenv("PRS_L8");
+        ctx->no_l8 = l8 && l8[0] == '0';
     }
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;
