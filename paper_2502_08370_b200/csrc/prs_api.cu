@@ -25,6 +25,7 @@
 #include "lpass5.cuh"
 #include "xpass6.cuh"
 #include "lpass8.cuh"
+#include "lpass9.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -118,6 +119,10 @@ struct prs_ctx {
     bool no_fused = false;  // PRS_FUSED=0: 2-D long lines take xpass3 + lpass5 (A/B measurements)
     bool fused_notup = false;  // PRS_FUSED=2: xpass6 without the fused y tuples + lp5 tuple kernel
     bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
+    bool no_tiled = true;      // PRS_TILED=1: 2-D long lines take lp9 x tiles + lp8 (opt-in:
+                               // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
+    double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
+    size_t l9_bytes = 0;
     double *l5buf = nullptr;  // lpass5 block tuples and block y/x
     size_t l5_bytes = 0;
     std::string err;
@@ -729,6 +734,134 @@ static int launch_fused2d(prs_ctx *ctx, int scheme, const TauFactors &f, const d
     return PRS_OK;
 }
 
+// 2-D long lines (n = 2048 / 4096): both stages as 64 x 64 tile kernels persistent over slice
+// groups: x tuples (lp9 MODE 0), x scan, x finish + y tuples (lp9 MODE 1) -> r_2 in `out`,
+// y scan, y finish + epilogue (lp8 MODE 1) in place.
+static bool tiled2d_ok(const prs_ctx *ctx) {
+    const int n = ctx->p.n;
+    return !ctx->no_tiled && fused2d_ok(ctx) == false && !ctx->force_v2 && !ctx->force_l3 && !ctx->no_l8 &&
+           ctx->p.dim == 2 && ctx->p.split == 0 && (n == 2048 || n == 4096);
+}
+
+static int launch_tiled2d(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out, long long B,
+                          const TimeArgs &ta, const EpiArgs &ep, bool prof, long long stride) {
+    const int n = ctx->p.n;
+    const int nb = n / L5W;  // blocks per line (square tiles: nrb = ncb)
+    const long long ts = B * (long long)nb * n;
+    const size_t need = sizeof(double) * 14 * (size_t)ts;  // 5 + 2 (x), 5 + 2 (y)
+    if (ctx->l9_bytes < need) {
+        if (ctx->l9buf) CK(cudaFree(ctx->l9buf));
+        ctx->l9buf = nullptr;
+        CK(cudaMalloc(&ctx->l9buf, need));
+        ctx->l9_bytes = need;
+    }
+    double *ttx = ctx->l9buf, *yxx = ttx + 5 * ts, *tty = yxx + 2 * ts, *yxy = tty + 5 * ts;
+    const int coef = ctx->p.coef_kind, dr = (scheme == PRS_DR) ? 1 : 0, src = ctx->p.source_kind;
+    const CoefTab tab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    L9Args x{};
+    x.in = in;
+    x.out = out;
+    x.vol = stride;
+    x.n = n;
+    x.nrb = nb;
+    x.ncb = nb;
+    x.nsq = B;
+    x.s8 = (int)std::min<long long>(B, 16);
+    x.nsg8 = (int)((B + x.s8 - 1) / x.s8);
+    x.tau = f.tau;
+    x.h2inv = ctx->h2inv;
+    x.creact = ctx->creact;
+    x.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
+    x.sinpi = ctx->sinpi;
+    x.ta = ta;
+    x.tab = tab;
+    x.invdx = f.invdx;
+    x.invdy = f.invdy;
+    x.s2n = ctx->s2n;
+    x.s2f = ctx->s2f;
+    x.ttx = ttx;
+    x.yxx = yxx;
+    x.tsx = ts;
+    x.tty = tty;
+    x.tsy = ts;
+    void (*k0)(L9Args) = nullptr, *k1v = nullptr;
+    void (*k1)(L9Args) = nullptr;
+    (void)k1v;
+#define XK(C, D, S_)                                   \
+    if (coef == C && dr == D && src == S_) {           \
+        k0 = lp9_kernel<C, D, S_, 0>;                  \
+        k1 = lp9_kernel<C, D, S_, 1>;                  \
+    }
+    XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
+#undef XK
+    const size_t shm9 = lpass9_smem_bytes();
+    CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm9));
+    CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm9));
+    const long long grid = (long long)nb * nb * x.nsg8;
+    // scans: lines of nb blocks, n lines per state
+    L5Args sx{};
+    sx.n = n;
+    sx.nrb = nb;
+    sx.tt = ttx;
+    sx.yx = yxx;
+    sx.tstride = ts;
+    const long long nlines = B * (long long)n;
+    if (prof) TRY(prof_begin(ctx));
+    k0<<<(unsigned)grid, L5T, shm9, ctx->stream>>>(x);
+    TRY(last_launch(ctx));
+    lp5_scan_kernel<<<(unsigned)((nlines + 255) / 256), 256, 0, ctx->stream>>>(sx, nlines);
+    TRY(last_launch(ctx));
+    k1<<<(unsigned)grid, L5T, shm9, ctx->stream>>>(x);
+    TRY(last_launch(ctx));
+    if (prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * (16.0 + (coef ? 8.0 : 0.0))));
+    // y stage
+    L5Args a{};
+    a.in = out;
+    a.out = out;
+    a.vol = stride;
+    a.n = n;
+    a.Sl = n;
+    a.nq = 1;
+    a.Sq = (long long)n * n;
+    a.nrb = nb;
+    a.ncb = nb;
+    a.nsq = B;
+    a.ntiles = B * nb * nb;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.tab = tab;
+    a.invd = f.invdy;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    a.tstride = ts;
+    a.tt = tty;
+    a.yx = yxy;
+    a.e_gc = ep.gc;
+    a.e_gcache = ep.gcache;
+    a.e_delta = ep.delta;
+    a.e_traj = ep.traj;
+    a.e_red = ctx->red;
+    a.s8 = x.s8;
+    a.nsg8 = x.nsg8;
+    void (*f8)(L5Args) = nullptr;
+#define LK(C, E) if (coef == C && ep.kind == E) f8 = lp8_kernel<C, E, 1>;
+    LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
+#undef LK
+    const size_t shm8 = lpass8_smem_bytes();
+    CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm8));
+    if (prof) TRY(prof_begin(ctx));
+    lp5_scan_kernel<<<(unsigned)((nlines + 255) / 256), 256, 0, ctx->stream>>>(a, nlines);
+    TRY(last_launch(ctx));
+    f8<<<(unsigned)grid, L5T, shm8, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    if (prof) {
+        double per = 16.0 + (coef ? 8.0 : 0.0);
+        if (ep.kind == EPI_DELTA) per += 8.0;
+        TRY(prof_end(ctx, PRS_K_LPASS, (double)B * (double)ctx->vol * per));
+    }
+    return PRS_OK;
+}
+
 // One step of `scheme` on B consecutive states: in -> out (out holds the result, or the
 // epilogue consumes it).  tmp must be distinct from in when scheme is DR.
 static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
@@ -738,6 +871,7 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
                        ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err, ctx->launches,
                        2.0 * M_PI * M_PI + ctx->p.c - 1.0, ctx->p.source_kind);
     if (fused2d_ok(ctx)) return launch_fused2d(ctx, scheme, f, in, out, B, ta, ep, prof, stride);
+    if (tiled2d_ok(ctx)) return launch_tiled2d(ctx, scheme, f, in, out, B, ta, ep, prof, stride);
     if (stride != ctx->vol) {
         ctx->err = "internal: padded slice stride on a path without stride support";
         return PRS_EUNSUPPORTED;
@@ -866,6 +1000,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *l9 = getenv("PRS_TILED");
+        ctx->no_tiled = !(l9 && l9[0] == '1');
     }
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;
@@ -961,6 +1097,7 @@ void prs_destroy(prs_ctx *ctx) {
     if (ctx->red) cudaFree(ctx->red);
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
     if (ctx->l5buf) cudaFree(ctx->l5buf);
+    if (ctx->l9buf) cudaFree(ctx->l9buf);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
