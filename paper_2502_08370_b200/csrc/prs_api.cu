@@ -123,6 +123,13 @@ struct prs_ctx {
                                // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
     double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
     size_t l9_bytes = 0;
+    // CUDA graphs of the per-iteration launch sequences (single rank, profiling off): the
+    // fine sweep and the coarse correction chain are captured on their second call (the first
+    // one allocates lazily-sized scratch) and replayed afterwards.  PRS_GRAPHS=0 disables.
+    bool graphs = true;
+    int fine_calls = 0, corr_calls = 0;
+    cudaGraphExec_t fine_exec = nullptr, corr_exec = nullptr;
+    long long fine_glaunch = 0, corr_glaunch = 0;  // kernels per replay
     double *l5buf = nullptr;  // lpass5 block tuples and block y/x
     size_t l5_bytes = 0;
     std::string err;
@@ -784,9 +791,8 @@ static int launch_tiled2d(prs_ctx *ctx, int scheme, const TauFactors &f, const d
     x.tsx = ts;
     x.tty = tty;
     x.tsy = ts;
-    void (*k0)(L9Args) = nullptr, *k1v = nullptr;
+    void (*k0)(L9Args) = nullptr;
     void (*k1)(L9Args) = nullptr;
-    (void)k1v;
 #define XK(C, D, S_)                                   \
     if (coef == C && dr == D && src == S_) {           \
         k0 = lp9_kernel<C, D, S_, 0>;                  \
@@ -1000,6 +1006,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *gv = getenv("PRS_GRAPHS");
+        ctx->graphs = !(gv && gv[0] == '0');
         const char *l9 = getenv("PRS_TILED");
         ctx->no_tiled = !(l9 && l9[0] == '1');
     }
@@ -1098,6 +1106,8 @@ void prs_destroy(prs_ctx *ctx) {
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
     if (ctx->l5buf) cudaFree(ctx->l5buf);
     if (ctx->l9buf) cudaFree(ctx->l9buf);
+    if (ctx->fine_exec) cudaGraphExecDestroy(ctx->fine_exec);
+    if (ctx->corr_exec) cudaGraphExecDestroy(ctx->corr_exec);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1154,10 +1164,7 @@ int prs_coarse_sweep(prs_ctx *ctx) {
     return PRS_OK;
 }
 
-int prs_fine_sweep(prs_ctx *ctx) {
-    if (!ctx) return PRS_EINVAL;
-    if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
-    TRY(ensure_factors(ctx, 1, ctx->dt));
+static int enqueue_fine_sweep(prs_ctx *ctx) {
     const int s = ctx->p.s;
     const double *src = ctx->traj;
     double *bufs[2] = {ctx->fa, ctx->fb};
@@ -1175,18 +1182,60 @@ int prs_fine_sweep(prs_ctx *ctx) {
         }
         TRY(run_step(ctx, ctx->p.F, ctx->fac[1], src, dst, ctx->count, ta, ep, ctx->prof, ctx->ss));
         src = dst;
-        ctx->delta = dst;
     }
+    return PRS_OK;
+}
+
+// Run `enqueue` directly, or (single rank, profiling off, from the second call on) as a replay
+// of its captured CUDA graph.  Kernel arguments are the context's fixed buffers, so one
+// capture serves every later call.
+static int run_graphed(prs_ctx *ctx, int (*enqueue)(prs_ctx *), int &calls, cudaGraphExec_t &exec,
+                       long long &per_replay) {
+    const bool use = ctx->graphs && ctx->nranks == 1 && !ctx->prof;
+    if (!use || calls++ == 0) return enqueue(ctx);
+    if (!exec) {
+        const long long l0 = ctx->launches;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue(ctx);
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+        if (rc != PRS_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e);
+            return PRS_ECUDA;
+        }
+        e = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            exec = nullptr;
+            ctx->err = std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e);
+            return PRS_ECUDA;
+        }
+        per_replay = ctx->launches - l0;
+        ctx->launches = l0;
+    }
+    CK(cudaGraphLaunch(exec, ctx->stream));
+    ctx->launches += per_replay;
+    return PRS_OK;
+}
+
+int prs_fine_sweep(prs_ctx *ctx) {
+    if (!ctx) return PRS_EINVAL;
+    if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
+    TRY(ensure_factors(ctx, 1, ctx->dt));
+    TRY(run_graphed(ctx, enqueue_fine_sweep, ctx->fine_calls, ctx->fine_exec, ctx->fine_glaunch));
+    ctx->delta = (ctx->p.s & 1) ? ctx->fa : ctx->fb;
     if (ctx->prof) TRY(prof_flush(ctx));
     return PRS_OK;
 }
 
-int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
-    if (!ctx) return PRS_EINVAL;
-    if (!ctx->delta) { ctx->err = "prs_fine_sweep first"; return PRS_EINVAL; }
+// the local part of the coarse correction chain: G step + fused correction
+// epilogue for every local slice, in time order
+static int enqueue_correct_chain(prs_ctx *ctx) {
     CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
-    if (ctx->nranks > 1 && ctx->rank > 0)
-        NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
     for (int i = 0; i < ctx->count; ++i) {
         EpiArgs ep;
         ep.kind = EPI_CORRECT;
@@ -1195,6 +1244,28 @@ int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
         ep.traj = state(ctx, ctx->traj, i + 1);
         TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
                      coarse_time(ctx, ctx->first + i), ep, false, ctx->ss));
+    }
+    return PRS_OK;
+}
+
+int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
+    if (!ctx) return PRS_EINVAL;
+    if (!ctx->delta) { ctx->err = "prs_fine_sweep first"; return PRS_EINVAL; }
+    if (ctx->nranks > 1) {
+        CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
+        if (ctx->rank > 0)
+            NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+        for (int i = 0; i < ctx->count; ++i) {
+            EpiArgs ep;
+            ep.kind = EPI_CORRECT;
+            ep.gcache = state(ctx, ctx->gcache, i);
+            ep.delta = state(ctx, ctx->delta, i);
+            ep.traj = state(ctx, ctx->traj, i + 1);
+            TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
+                         coarse_time(ctx, ctx->first + i), ep, false, ctx->ss));
+        }
+    } else {
+        TRY(run_graphed(ctx, enqueue_correct_chain, ctx->corr_calls, ctx->corr_exec, ctx->corr_glaunch));
     }
     if (ctx->nranks > 1) {
         if (ctx->rank < ctx->nranks - 1)

@@ -450,3 +450,22 @@ def test_fine_solve_matches_sequential_fine_solution(p):
     ctx.fine_solve(np.ascontiguousarray(u0), hout, p.N)
     assert float(np.max(np.abs(hout - want[p.N]))) / scale <= TOL
     ctx.close()
+
+
+@pytest.mark.parametrize("p", [synth.CONFIGS["c0"],
+                               Problem(dim=2, n=64, c=1.0, coef=1, N=6, s=4, G=FIE, F=DR, init="modes", seed=2),
+                               Problem(dim=3, n=24, c=1.0, source=1, N=4, s=3),
+                               Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=4,
+                                       s=3, G=DR, F=FIE)],
+                         ids=lambda p: p.label())
+def test_graph_replay_bitwise_equals_direct_launches(p, monkeypatch):
+    """Iterations 2.. replay captured CUDA graphs of the fine sweep and the correction chain;
+    they must reproduce the directly launched kernels bit for bit (PRS_GRAPHS=0)."""
+    u0 = synth.initial_state(p)
+    runs = []
+    for g in ("1", "0"):
+        monkeypatch.setenv("PRS_GRAPHS", g)
+        trajs, upds = gpu_parareal(p, u0, min(p.N, 4))
+        runs.append((np.stack(trajs), upds))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
