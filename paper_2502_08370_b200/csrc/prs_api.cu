@@ -26,6 +26,7 @@
 #include "xpass6.cuh"
 #include "lpass8.cuh"
 #include "lpass9.cuh"
+#include "xy3.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -119,6 +120,7 @@ struct prs_ctx {
     bool no_fused = false;  // PRS_FUSED=0: 2-D long lines take xpass3 + lpass5 (A/B measurements)
     bool fused_notup = false;  // PRS_FUSED=2: xpass6 without the fused y tuples + lp5 tuple kernel
     bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
+    bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
     bool no_tiled = true;      // PRS_TILED=1: 2-D long lines take lp9 x tiles + lp8 (opt-in:
                                // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
     double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
@@ -882,6 +884,40 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
         ctx->err = "internal: padded slice stride on a path without stride support";
         return PRS_EUNSUPPORTED;
     }
+    if (ctx->p.dim == 3 && ctx->p.n == XY_N && ctx->p.coef_kind == 0 && scheme == PRS_FIE && !ctx->no_xy &&
+        !ctx->force_v2) {
+        // x and y stages fused per z-plane (xy3.cuh), then the z stage
+        XYArgs x{};
+        x.in = in;
+        x.out = out;
+        x.vol = ctx->vol;
+        x.nplanes = B * XY_N;
+        x.tau = f.tau;
+        x.src_amp = 3.0 * M_PI * M_PI + ctx->p.c - 1.0;
+        x.sinpi = ctx->sinpi;
+        x.ta = ta;
+        x.tab = CoefTab{f.tab, f.tab + XY_N, f.tab + 2 * XY_N};
+        void (*kx)(XYArgs) = ctx->p.source_kind ? xy3_kernel<1> : xy3_kernel<0>;
+        const size_t shm = xy3_smem_bytes();
+        CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(2 * x.nplanes));
+        cfg.blockDim = dim3(XY_T);
+        cfg.dynamicSmemBytes = shm;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (prof) TRY(prof_begin(ctx));
+        CK(cudaLaunchKernelEx(&cfg, kx, x));
+        TRY(last_launch(ctx));
+        if (prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * 16.0));
+        return launch_lpass(ctx, 2, f, out, out, B, ep, prof);
+    }
     TRY(launch_xpass(ctx, scheme, f, in, out, B, ta, prof));
     if (ctx->p.dim == 2) return launch_lpass(ctx, 1, f, out, out, B, ep, prof);
     EpiArgs st;
@@ -1006,6 +1042,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *xyv = getenv("PRS_XY");
+        ctx->no_xy = xyv && xyv[0] == '0';
         const char *gv = getenv("PRS_GRAPHS");
         ctx->graphs = !(gv && gv[0] == '0');
         const char *l9 = getenv("PRS_TILED");

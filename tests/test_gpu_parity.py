@@ -469,3 +469,31 @@ def test_graph_replay_bitwise_equals_direct_launches(p, monkeypatch):
         runs.append((np.stack(trajs), upds))
     assert np.array_equal(runs[0][0], runs[1][0])
     assert runs[0][1] == runs[1][1]
+
+
+@pytest.mark.parametrize("mode", ["xy", "separate"])
+def test_c2_shape_xy_fused_plane_path(mode, monkeypatch):
+    """3-D n = 128 (c2's plane size): x and y stages fused per z-plane in a 2-CTA cluster
+    (xy3.cuh) vs the oracle, batched steps over several states and a parareal run; PRS_XY=0
+    runs the separate x / y passes."""
+    if mode == "separate":
+        monkeypatch.setenv("PRS_XY", "0")
+    p = Problem(dim=3, n=128, c=1.0, source=1, N=2, s=2, G=FIE, F=FIE)
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    o = oracle.Oracle(p)
+    B = 3
+    base = synth.initial_state(p)
+    us = np.stack([base * (1.0 + 0.5 * b) + 1e-2 * rand_field(p, 70 + b) for b in range(B)])
+    du = dev(us)
+    out = torch.empty_like(du)
+    dt, dT = p.T / (p.N * p.s), p.T / p.N
+    for which, j in ((1, 1), (0, 0)):
+        ctx.step_batch(which, 0, j, du, out, B)
+        got = host(out)
+        for b in range(B):
+            tau, tn = (dt, float(b * p.s + j + 1) * dt) if which == 1 else (dT, float(b + 1) * dT)
+            want = o.step(FIE, tau, tn, us[b])
+            assert nerr(got[b], want, want, us[b]) <= TOL, (which, b)
+    ctx.close()
+    _parareal_vs_oracle(p)
