@@ -68,6 +68,9 @@ CONFIGS = {
     # c3: 2-D 4096^2, variable kappa, G = FIE (paper's L-stable coarse), F = DR, N = 64, s = 256
     "c3": Problem(dim=2, n=4096, c=1.0, coef=1, source=0, N=64, s=256, G=FIE, F=DR,
                   init="modes"),
+    # c1p: c1 with the paper's own pairing Parareal/FIE-DR
+    # (G = FIE, L-stable; F = DR)
+    "c1p": Problem(dim=2, n=256, c=1.0, source=0, N=32, s=64, G=FIE, F=DR, init="modes"),
     # c4: 2-D 1024^2 DD, 8 strips, 8-cell overlap, linear ramp, manufactured, N = 32, s = 64
     "c4": Problem(dim=2, n=1024, c=1.0, split=1, dd_strips=8, dd_overlap=8, dd_ramp=0,
                   source=1, N=32, s=64, G=FIE, F=FIE, init="phi"),

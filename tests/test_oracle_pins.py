@@ -467,3 +467,24 @@ def test_determinism():
     a, _ = o.parareal(u0, 2, fixed=True)
     b, _ = o.parareal(u0, 2, fixed=True)
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_c1_paper_pairing_fie_dr_contracts_per_mode():
+    """NEXT-1: on c1's 16 excited modes the paper's pairing Parareal/FIE-DR
+    has convergence factor K < 1 (Theorem), and the error of each mode's
+    parareal iterate against its fine solution contracts at least like K^k.
+    Scalar recurrences in mpmath; the GPU field is checked against their superposition in
+    test_gpu_parity.py."""
+    p = synth.CONFIGS["c1p"]
+    dT = mp.mpf(p.T) / p.N
+    for j, l, _a in synth.mode_table(p.seed):
+        lam = modal.lambdas((j, l), p.n, p.c, 2)
+        K = float(modal.conv_factor([dT * x for x in lam], p.s, "FIE", "DR"))
+        assert K < 1.0, (j, l, K)
+        sp = modal.ScalarParareal(lam, p.T, p.N, p.s, FIE, DR)
+        fine = sp.fine_solution(1)
+        trs = sp.run(1, 4)
+        e0 = max(abs(x - y) for x, y in zip(trs[0][1:], fine[1:]))
+        for k in range(1, 5):
+            ek = max(abs(x - y) for x, y in zip(trs[k][1:], fine[1:]))
+            assert float(ek) <= K ** k * float(e0) * (1 + 1e-9) + 1e-30, (j, l, k, float(ek), K)
