@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/prs.h"
@@ -416,19 +417,35 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     const double *idy = a.idy[blk];
     constexpr int NMR = (DD_WMAX + 31) / 32;
     double Ain[NMR], Bin[NMR];
+    // The walks below come in a predicated form (partial last chunk) and an unpredicated one
+    // for full chunks (every chunk of c4); the line's first and last rows (m = 0 / cc = 0)
+    // are the only boundary cases and are tested once per walk.
+    const int lb = r0 + e0;  // global row of the chunk's first element
+    const bool full = (cnt == LCH);
+    // multiplier of element i (row lb + i): m = -tau/h^2 * id(row - 1); 0 on the line's first row
+    auto mrow = [&](const double *ip, int i) {
+        return (i == 0 && lb == 0) ? 0.0 : ms * __ldg(ip + (long long)(i - 1) * W);
+    };
+    auto f1 = [&](auto FT, int am, double &A, double &B) {
+        constexpr bool FULL = decltype(FT)::value;
+        const double *ip = idy + (long long)lb * W + am;
+        A = 1.0;
+        B = 0.0;
+#pragma unroll
+        for (int i = 0; i < LCH; ++i)
+            if (FULL || i < cnt) {
+                const double m = mrow(ip, i);
+                B = fma(-m, B, T[cpad(e0 + i) * DD_WPAD + am]);
+                A = -m * A;
+            }
+    };
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
         const int am = lane + 32 * rr;
         double A = 1.0, B = 0.0;
         if (am < W) {
-#pragma unroll
-            for (int i = 0; i < LCH; ++i)
-                if (i < cnt) {
-                    const int l = r0 + e0 + i;
-                    const double m = (l > 0) ? ms * __ldg(idy + (long long)(l - 1) * W + am) : 0.0;
-                    B = fma(-m, B, T[cpad(e0 + i) * DD_WPAD + am]);
-                    A = -m * A;
-                }
+            if (full) f1(std::true_type{}, am, A, B);
+            else f1(std::false_type{}, am, A, B);
             sc[t * DD_WMAX + am] = make_double2(A, B);
         }
         Ain[rr] = A;
@@ -480,24 +497,31 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     for (int rr = 0; rr < NMR; ++rr) yin[rr] = fma(Ain[rr], Ycta[rr], Bin[rr]);
     __syncthreads();
     // F3 + backward composition
+    auto f3 = [&](auto FT, int am, double y, double &Pb, double &Qb) {
+        constexpr bool FULL = decltype(FT)::value;
+        const double *ip = idy + (long long)lb * W + am;
+        Pb = 1.0;
+        Qb = 0.0;
+#pragma unroll
+        for (int i = 0; i < LCH; ++i)
+            if (FULL || i < cnt) {
+                const double m = mrow(ip, i);
+                const double id = __ldg(ip + (long long)i * W);
+                const double ccv = (lb + i == n - 1) ? 0.0 : ms * id;
+                double *p = T + cpad(e0 + i) * DD_WPAD + am;
+                y = fma(-m, y, *p);
+                *p = y;
+                Qb = fma(Pb * id, y, Qb);
+                Pb *= -ccv;
+            }
+    };
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
         const int am = lane + 32 * rr;
         if (am < W) {
-            double y = yin[rr], Pb = 1.0, Qb = 0.0;
-#pragma unroll
-            for (int i = 0; i < LCH; ++i)
-                if (i < cnt) {
-                    const int l = r0 + e0 + i;
-                    const double m = (l > 0) ? ms * __ldg(idy + (long long)(l - 1) * W + am) : 0.0;
-                    const double id = __ldg(idy + (long long)l * W + am);
-                    const double ccv = (l < n - 1) ? ms * id : 0.0;
-                    double *p = T + cpad(e0 + i) * DD_WPAD + am;
-                    y = fma(-m, y, *p);
-                    *p = y;
-                    Qb = fma(Pb * id, y, Qb);
-                    Pb *= -ccv;
-                }
+            double Pb, Qb;
+            if (full) f3(std::true_type{}, am, yin[rr], Pb, Qb);
+            else f3(std::false_type{}, am, yin[rr], Pb, Qb);
             sc[t * DD_WMAX + am] = make_double2(Pb, Qb);
         }
     }
@@ -546,21 +570,25 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) xin[rr] = fma(Ain[rr], Xcta[rr], Bin[rr]);
     // B3
+    auto b3 = [&](auto FT, int am, double x) {
+        constexpr bool FULL = decltype(FT)::value;
+        const double *ip = idy + (long long)lb * W + am;
+#pragma unroll
+        for (int i = LCH - 1; i >= 0; --i)
+            if (FULL || i < cnt) {
+                const double id = __ldg(ip + (long long)i * W);
+                const double ccv = (lb + i == n - 1) ? 0.0 : ms * id;
+                double *p = T + cpad(e0 + i) * DD_WPAD + am;
+                x = fma(id, *p, -ccv * x);
+                *p = x;
+            }
+    };
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
         const int am = lane + 32 * rr;
         if (am < W) {
-            double x = xin[rr];
-#pragma unroll
-            for (int i = LCH - 1; i >= 0; --i)
-                if (i < cnt) {
-                    const int l = r0 + e0 + i;
-                    const double id = __ldg(idy + (long long)l * W + am);
-                    const double ccv = (l < n - 1) ? ms * id : 0.0;
-                    double *p = T + cpad(e0 + i) * DD_WPAD + am;
-                    x = fma(id, *p, -ccv * x);
-                    *p = x;
-                }
+            if (full) b3(std::true_type{}, am, xin[rr]);
+            else b3(std::false_type{}, am, xin[rr]);
         }
     }
     // ---- U = V Q^T ----
