@@ -132,6 +132,12 @@ struct prs_ctx {
     int fine_calls = 0, corr_calls = 0;
     cudaGraphExec_t fine_exec = nullptr, corr_exec = nullptr;
     long long fine_glaunch = 0, corr_glaunch = 0;  // kernels per replay
+    // prs_iterate: slices n < kconv are converged (U^k_n exact and bitwise frozen for n <= k,
+    // PAPER.md:214), so their fine propagation and coarse correction would reproduce the
+    // previous iteration's Delta_n and U_{n+1}: they are skipped.  Enabled for states of
+    // >= 2^18 points (PRS_SKIP=0/1 overrides); bare fine_sweep / correct calls never skip.
+    bool skip_converged = false;
+    int kconv = 0;
     double *l5buf = nullptr;  // lpass5 block tuples and block y/x
     size_t l5_bytes = 0;
     std::string err;
@@ -1044,6 +1050,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->no_l8 = l8 && l8[0] == '0';
         const char *xyv = getenv("PRS_XY");
         ctx->no_xy = xyv && xyv[0] == '0';
+        const char *sv = getenv("PRS_SKIP");
+        ctx->skip_converged = sv ? (sv[0] == '1') : (ctx->vol >= (1LL << 18));
         const char *gv = getenv("PRS_GRAPHS");
         ctx->graphs = !(gv && gv[0] == '0');
         const char *l9 = getenv("PRS_TILED");
@@ -1202,23 +1210,32 @@ int prs_coarse_sweep(prs_ctx *ctx) {
     return PRS_OK;
 }
 
+// first local slice that still needs work (prs_iterate's converged prefix, else 0)
+static int local_start(const prs_ctx *ctx) {
+    const int k = ctx->kconv - ctx->first;
+    return k <= 0 ? 0 : (k > ctx->count ? ctx->count : k);
+}
+
 static int enqueue_fine_sweep(prs_ctx *ctx) {
     const int s = ctx->p.s;
-    const double *src = ctx->traj;
-    double *bufs[2] = {ctx->fa, ctx->fb};
+    const int i0 = local_start(ctx);
+    const long long B = ctx->count - i0;
+    if (B <= 0) return PRS_OK;
+    const double *src = state(ctx, ctx->traj, i0);
+    double *bufs[2] = {state(ctx, ctx->fa, i0), state(ctx, ctx->fb, i0)};
     for (int j = 0; j < s; ++j) {
         double *dst = bufs[j & 1];
         TimeArgs ta;
-        ta.slice0 = ctx->first;
+        ta.slice0 = ctx->first + i0;
         ta.tmul = s;
         ta.toff = j + 1;
         ta.tstep = ctx->dt;
         EpiArgs ep;
         if (j == s - 1) {
             ep.kind = EPI_DELTA;
-            ep.gc = ctx->gcache;
+            ep.gc = state(ctx, ctx->gcache, i0);
         }
-        TRY(run_step(ctx, ctx->p.F, ctx->fac[1], src, dst, ctx->count, ta, ep, ctx->prof, ctx->ss));
+        TRY(run_step(ctx, ctx->p.F, ctx->fac[1], src, dst, B, ta, ep, ctx->prof, ctx->ss));
         src = dst;
     }
     return PRS_OK;
@@ -1229,7 +1246,8 @@ static int enqueue_fine_sweep(prs_ctx *ctx) {
 // capture serves every later call.
 static int run_graphed(prs_ctx *ctx, int (*enqueue)(prs_ctx *), int &calls, cudaGraphExec_t &exec,
                        long long &per_replay) {
-    const bool use = ctx->graphs && ctx->nranks == 1 && !ctx->prof;
+    // (graphs are captured for the full batch: a converged prefix launches directly)
+    const bool use = ctx->graphs && ctx->nranks == 1 && !ctx->prof && local_start(ctx) == 0;
     if (!use || calls++ == 0) return enqueue(ctx);
     if (!exec) {
         const long long l0 = ctx->launches;
@@ -1274,7 +1292,7 @@ int prs_fine_sweep(prs_ctx *ctx) {
 // epilogue for every local slice, in time order
 static int enqueue_correct_chain(prs_ctx *ctx) {
     CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
-    for (int i = 0; i < ctx->count; ++i) {
+    for (int i = local_start(ctx); i < ctx->count; ++i) {
         EpiArgs ep;
         ep.kind = EPI_CORRECT;
         ep.gcache = state(ctx, ctx->gcache, i);
@@ -1293,7 +1311,7 @@ int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
         CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
         if (ctx->rank > 0)
             NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-        for (int i = 0; i < ctx->count; ++i) {
+        for (int i = local_start(ctx); i < ctx->count; ++i) {
             EpiArgs ep;
             ep.kind = EPI_CORRECT;
             ep.gcache = state(ctx, ctx->gcache, i);
@@ -1331,7 +1349,10 @@ int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
     int k = 0;
     int rc = PRS_OK;
     for (; k < K;) {
-        TRY(prs_fine_sweep(ctx));
+        // iteration k computes U^{k+1}; slices n < k are converged (see kconv)
+        ctx->kconv = ctx->skip_converged ? k : 0;
+        rc = prs_fine_sweep(ctx);
+        if (rc != PRS_OK) break;
         double upd = 0.0;
         rc = prs_parareal_correct(ctx, &upd);
         if (hist) hist[k] = upd;
@@ -1339,6 +1360,7 @@ int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
         if (rc != PRS_OK) break;
         if (upd <= tol) break;
     }
+    ctx->kconv = 0;
     if (k_out) *k_out = k;
     return rc;
 }

@@ -520,3 +520,35 @@ def test_c1_paper_pairing_full_size_matches_modal_closed_form():
         assert float(np.max(np.abs(gtrajs[k] - want))) / scale <= TOL, k
     # the update norm falls (the paper's pairing converges; c1's DR-DR pairing does not, R11)
     assert gupds[-1] < gupds[0]
+
+
+@pytest.mark.parametrize("p", [Problem(dim=2, n=96, c=1.0, coef=1, N=8, s=4, G=FIE, F=DR, init="modes", seed=4),
+                               Problem(dim=3, n=128, c=1.0, source=1, N=6, s=2, G=FIE, F=FIE),
+                               Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=6,
+                                       s=3, G=FIE, F=FIE),
+                               Problem(dim=2, n=2048, c=1.0, coef=1, N=4, s=2, G=FIE, F=DR, init="modes", seed=5)],
+                         ids=lambda p: p.label())
+def test_iterate_skipping_converged_slices_is_bitwise_neutral(p, monkeypatch):
+    """prs_iterate skips slices n < k at iteration k (exact after k iterations, PAPER.md:214,
+    and bitwise frozen): trajectory and update history equal the full iteration's bit for bit."""
+    prs = prs_mod()
+    u0 = synth.initial_state(p)
+    outs = []
+    for sk in ("1", "0"):
+        monkeypatch.setenv("PRS_SKIP", sk)
+        ctx = prs.Context(p)
+        ctx.set_initial(dev(u0))
+        ctx.coarse_sweep()
+        k, hist = ctx.iterate(p.N, 0.0)
+        buf = torch.empty((p.n,) * p.dim, dtype=torch.float64, device="cuda")
+        traj = np.stack([host(ctx.get_slice(n, buf)).copy() for n in range(p.N + 1)])
+        ctx.close()
+        outs.append((k, hist, traj))
+    assert outs[0][0] == outs[1][0] == p.N
+    assert outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][2], outs[1][2])
+    # and the result is the sequential fine solution (finite termination)
+    fine = oracle.Oracle(p).fine_solution(u0) if p.n <= 128 else None
+    if fine is not None:
+        scale = max(float(np.max(np.abs(t))) for t in fine)
+        assert float(np.max(np.abs(outs[0][2] - fine))) / scale <= TOL
