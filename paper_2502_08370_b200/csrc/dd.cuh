@@ -46,7 +46,7 @@ constexpr int DD_RMAX = 128;   // rows per CTA
 constexpr int DD_WMAX = 144;   // widest block (16 column groups x 9)
 constexpr int DD_WPAD = 148;   // shared row stride of a tile (>= DD_WMAX, == 4 mod 16)
 constexpr int DD_KC = 16;      // Q rows staged per k-chunk
-constexpr int DD_THREADS = 256;
+constexpr int DD_THREADS = 512;  // 16 warps: 32 row groups x 16 column groups in the GEMMs
 
 // ------------------------------------------------------------- partition of unity --
 // rho_0 at a 1-based position xpos (integer = node, half-integer = face), index-space
@@ -236,8 +236,8 @@ struct DDStageArgs {
 };
 
 // GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place.
-// 256 threads = 16 row groups x 16 column groups; each thread accumulates 8 rows (rg + 16 r)
-// x 9 columns (9 cg + j) in registers (72 fp64 FMAs per 17 shared loads per k).  M streams
+// 512 threads = 32 row groups x 16 column groups; each thread accumulates 4 rows (rg + 32 r)
+// x 9 columns (9 cg + j) in registers (36 fp64 FMAs per 13 shared loads per k).  M streams
 // through two shared k-chunks of DD_KC rows with cp.async (next chunk in flight while the
 // current one is consumed).  Columns >= W of T and of the staged M rows are zero, so the
 // inner loops need no predicates; rows >= nrow are computed and discarded.
@@ -263,9 +263,10 @@ __device__ __forceinline__ void dd_stage_mchunk(const double *M, int W, int k0, 
 __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
     const int tid = threadIdx.x;
     const int cg = tid & 15, rg = tid >> 4;
-    double acc[8][9];
+    constexpr int GR = DD_RMAX / (DD_THREADS / 16);  // rows per thread (4)
+    double acc[GR][9];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < GR; ++r)
 #pragma unroll
         for (int j = 0; j < 9; ++j) acc[r][j] = 0.0;
     const int nk = (W + DD_KC - 1) / DD_KC;
@@ -287,13 +288,13 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
         const double *mrow = cur + 9 * cg;
 #pragma unroll
         for (int kk = 0; kk < DD_KC; ++kk) {
-            double f[8], m[9];
+            double f[GR], m[9];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) f[r] = trow[cpad(rg + 16 * r) * DD_WPAD + kk];
+            for (int r = 0; r < GR; ++r) f[r] = trow[cpad(rg + (DD_THREADS / 16) * r) * DD_WPAD + kk];
 #pragma unroll
             for (int j = 0; j < 9; ++j) m[j] = mrow[kk * DD_WPAD + j];
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
+            for (int r = 0; r < GR; ++r)
 #pragma unroll
                 for (int j = 0; j < 9; ++j) acc[r][j] = fma(f[r], m[j], acc[r][j]);
         }
@@ -301,8 +302,8 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
     }
     // all reads of T are done (last barrier above): write in place
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const int l = rg + 16 * r;
+    for (int r = 0; r < GR; ++r) {
+        const int l = rg + (DD_THREADS / 16) * r;
         if (l < nrow) {
 #pragma unroll
             for (int j = 0; j < 9; ++j) {
@@ -409,13 +410,15 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     // ---- G = F Q ----
     dd_tile_gemm(T, a.Q[blk], W, nrow, Ms);
 
-    // ---- (theta_a I - tau Y) v_a = g_a along y: warp = chunk t, lanes = modes ----
-    const int t = tid >> 5, lane = tid & 31;
+    // ---- (theta_a I - tau Y) v_a = g_a along y: warp = chunk t (of 16 rows) x mode half,
+    // lanes = modes: half 0 walks mode rounds 0..2 (modes 0..95), half 1 rounds 3..4 ----
+    const int t = (tid >> 5) & 7, lane = tid & 31, mh = tid >> 8;
     const int e0 = t * LCH;
     const int cnt = max(0, min(LCH, nrow - e0));
     const double ms = -a.tau * a.h2inv;  // off-diagonal of theta I - tau Y
     const double *idy = a.idy[blk];
-    constexpr int NMR = (DD_WMAX + 31) / 32;
+    constexpr int NMR = 3;  // mode rounds per thread
+    const int rr0 = 3 * mh;  // first mode round of this half (round rr covers modes 32 rr .. 32 rr + 31)
     double Ain[NMR], Bin[NMR];
     // The walks below come in a predicated form (partial last chunk) and an unpredicated one
     // for full chunks (every chunk of c4); the line's first and last rows (m = 0 / cc = 0)
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     };
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
-        const int am = lane + 32 * rr;
+        const int am = lane + 32 * (rr0 + rr);
         double A = 1.0, B = 0.0;
         if (am < W) {
             if (full) f1(std::true_type{}, am, A, B);
@@ -456,7 +459,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     double yin[NMR];
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
-        const int am = lane + 32 * rr;
+        const int am = lane + 32 * (rr0 + rr);
         double EA = 1.0, EB = 0.0, TA = 1.0, TB = 0.0;  // exclusive prefix, CTA total
         if (am < W) {
             for (int q = 0; q < nch; ++q) {
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
         cl.sync();
 #pragma unroll
         for (int rr = 0; rr < NMR; ++rr) {
-            const int am = lane + 32 * rr;
+            const int am = lane + 32 * (rr0 + rr);
             if (am < W)
                 for (int r = 0; r < crank; ++r) {
                     const double2 v = cl.map_shared_rank(ctf, r)[am];
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     };
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
-        const int am = lane + 32 * rr;
+        const int am = lane + 32 * (rr0 + rr);
         if (am < W) {
             double Pb, Qb;
             if (full) f3(std::true_type{}, am, yin[rr], Pb, Qb);
@@ -529,7 +532,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     double xin[NMR];
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
-        const int am = lane + 32 * rr;
+        const int am = lane + 32 * (rr0 + rr);
         double EP = 1.0, EQ = 0.0, TP = 1.0, TQ = 0.0;
         if (am < W) {
             for (int q = nch - 1; q >= 0; --q) {
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
         cl.sync();
 #pragma unroll
         for (int rr = 0; rr < NMR; ++rr) {
-            const int am = lane + 32 * rr;
+            const int am = lane + 32 * (rr0 + rr);
             if (am < W)
                 for (int r = a.CL - 1; r > crank; --r) {
                     const double2 v = cl.map_shared_rank(ctb, r)[am];
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     };
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) {
-        const int am = lane + 32 * rr;
+        const int am = lane + 32 * (rr0 + rr);
         if (am < W) {
             if (full) b3(std::true_type{}, am, xin[rr]);
             else b3(std::false_type{}, am, xin[rr]);
