@@ -121,6 +121,7 @@ struct prs_ctx {
     bool fused_notup = false;  // PRS_FUSED=2: xpass6 without the fused y tuples + lp5 tuple kernel
     bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
+    bool x3_contig = false;    // PRS_X3CONTIG=1: xpass3 takes one contiguous range per CTA
     bool no_tiled = true;      // PRS_TILED=1: 2-D long lines take lp9 x tiles + lp8 (opt-in:
                                // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
     double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
@@ -301,6 +302,17 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.P = n / LCH;
     a.lines_per_state = (dim == 2) ? n : n * n;
     a.ngroups = B * ctx->vol / 4096;
+    a.nstates = (int)B;
+    // state-fastest ranges when every state has enough groups: the number of ranges makes
+    // B * nranges a multiple of the grid (balanced), each range >= 64 groups
+    a.nranges = 0;
+    if (!ctx->x3_contig && B > 1) {
+        const long long grid = std::min<long long>(ctx->num_sms, a.ngroups);
+        long long g = grid, bb = B;
+        while (bb) { const long long t = g % bb; g = bb; bb = t; }  // gcd(grid, B)
+        const long long R = grid / g;
+        if ((a.ngroups / B) / R >= 64) a.nranges = (int)R;
+    }
     a.dim = dim;
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
@@ -1048,6 +1060,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *x3c = getenv("PRS_X3CONTIG");
+        ctx->x3_contig = x3c && x3c[0] == '1';
         const char *xyv = getenv("PRS_XY");
         ctx->no_xy = xyv && xyv[0] == '0';
         const char *sv = getenv("PRS_SKIP");

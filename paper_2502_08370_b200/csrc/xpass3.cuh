@@ -30,6 +30,12 @@ struct X3Args {
     int P;                // chunks per line
     int lines_per_state;  // n^(dim-1)
     long long ngroups;    // batch * lines_per_state / (256 / P)
+    int nstates;          // batch size B
+    int nranges;          // > 0: each state's groups split into nranges contiguous ranges, tasks
+                          // (range, state) taken round-robin with the state fastest, so CTAs
+                          // running at the same time hold the same rows of different states and
+                          // the per-point pivot rows they share hit L2; 0: one contiguous range
+                          // of the whole batch per CTA
     int dim;
     double tau, h2inv, creact;
     double src_amp;
@@ -86,13 +92,24 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         tcc[i] = COEF ? 0.0 : __ldg(a.tab.cc + e0 + i);
     }
 
-    // ---- this CTA's contiguous range of groups ----
+    // ---- this CTA's ranges of groups ----
     const long long G = a.ngroups;
     const int lps_sh = __ffs(a.lines_per_state) - 1;  // lines per state is a power of two
-    const long long per = G / gridDim.x, rem = G % gridDim.x;
-    const long long g0 = blockIdx.x * per + min((long long)blockIdx.x, rem);
-    const long long g1 = g0 + per + (blockIdx.x < rem ? 1 : 0);
     const long long group_elems = (long long)X3T * LCH;  // 4096 doubles per group (contiguous)
+    const long long ntasks = a.nranges ? (long long)a.nranges * a.nstates : gridDim.x;
+    for (long long task = blockIdx.x; task < ntasks; task += gridDim.x) {
+    long long g0, g1;
+    if (a.nranges) {
+        const long long Gs = G / a.nstates;  // groups per state
+        const long long b = task % a.nstates, r = task / a.nstates;
+        g0 = b * Gs + (r * Gs) / a.nranges;
+        g1 = b * Gs + ((r + 1) * Gs) / a.nranges;
+    } else {
+        const long long per = G / gridDim.x, rem = G % gridDim.x;
+        g0 = task * per + min(task, rem);
+        g1 = g0 + per + (task < rem ? 1 : 0);
+    }
+    __syncthreads();  // the previous range's buffers are free
 
     // issue the 16-byte copies of group g of a row-major source into a chunk-layout buffer
     auto issue_group = [&](const double *src, long long g, double *dst) {
@@ -292,6 +309,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         __syncthreads();  // staging buffer free before the next prefetch lands in it
     }
     cp_async_wait<0>();
+    }  // tasks
 }
 
 }  // namespace prs
