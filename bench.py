@@ -44,6 +44,10 @@ def parse():
                          "run uses the BASELINE config unchanged)")
     ap.add_argument("--profile-launches", action="store_true",
                     help="under ncu: only a short run, no timing extras")
+    ap.add_argument("--coarse-mode", default="owner", choices=["owner", "space"],
+                    help="coarse chain: owner-G (default) or space-parallel G over P row bands "
+                         "(P = GPUs; --gbands virtual bands on one GPU)")
+    ap.add_argument("--gbands", type=int, default=4)
     ap.add_argument("--no-time-to-tol", action="store_true",
                     help="skip the parareal time-to-tolerance run and the sequential fine solve")
     return ap.parse_args()
@@ -211,6 +215,8 @@ def run_prs(args):
         uid = obj[0]
     stream = torch.cuda.current_stream()
     ctx = prs.Context(p, rank=rank, nranks=world, nccl_uid=uid, stream=stream.cuda_stream)
+    if args.coarse_mode == "space":
+        ctx.set_coarse_mode(1, world if world > 1 else args.gbands)
     u0 = synth.initial_state(p)
     u0_host = torch.from_numpy(u0).pin_memory()
     u0_dev = u0_host.cuda()
@@ -358,6 +364,7 @@ def run_prs(args):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": workload_config(p, args.config, world),
                 "parallelism": f"time-slices x{world}",
+                "coarse_mode": args.coarse_mode,
                 "updates": upds, "gpu_launches": launches, "clocks": clk, "roofline": roof,
                 "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt}
         print(json.dumps(line), flush=True)

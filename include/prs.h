@@ -116,6 +116,19 @@ int prs_step_batch(prs_ctx *ctx, int which, int slice0, int j, const double *in,
 int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices, double *out,
                    int out_on_device);
 
+/* Coarse-chain mode of prs_parareal_correct / prs_iterate (north star item 5).
+ * mode 0 (default): owner-G -- the G step of slice n runs on the GPU that owns slice n, the
+ *   chain hands U^{k+1}_n from rank to rank (ncclSend/Recv).
+ * mode 1: space-parallel G -- every coarse state is cut into P bands of n/P rows and all P
+ *   GPUs advance the chain together: the x stage of FIE is row-local, the y stage is a
+ *   partitioned tridiagonal solve (band block tuples, all-gathered band tuples, boundary
+ *   values per band); Delta_n bands are scattered from the slice owners before the chain and
+ *   the U_{n+1} / G-cache bands gathered back after it.  P = nranks; with one rank, `bands`
+ *   virtual bands run in the same process (tests the partitioned solve on one GPU).
+ *   Supported for the 2-D dimensional split with G = FIE, P and n powers of two, n <= 4096,
+ *   n % (64 P) == 0 (PRS_EUNSUPPORTED otherwise).  Results equal owner-G up to rounding. */
+int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands);
+
 /* Counters.  prs_launches: kernels this context has launched so far.  With profiling on,
  * every fine-sweep kernel launch is bracketed by CUDA events on the context stream and
  * prs_kernel_stats(kind) returns, for kind PRS_K_XPASS (contiguous-axis line solve),

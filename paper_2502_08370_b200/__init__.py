@@ -20,7 +20,7 @@ PRS_FIE, PRS_DR = 0, 1
 PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
 EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
-           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
+           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
            "prs_last_error", "prs_destroy"]
 
 
@@ -65,6 +65,7 @@ def lib() -> ctypes.CDLL:
             "prs_step": ([V, I, D, D, V, V], I),
             "prs_step_batch": ([V, I, I, I, V, V, I], I),
             "prs_fine_solve": ([V, V, I, I, V, I], I),
+            "prs_set_coarse_mode": ([V, I, I], I),
             "prs_set_profiling": ([V, I], I),
             "prs_launches": ([V], ctypes.c_longlong),
             "prs_kernel_stats": ([V, I, PL, PD, PD], I),
@@ -188,6 +189,11 @@ class Context:
         ns = self.prob.N if nslices is None else nslices
         self._check(self.L.prs_fine_solve(self.h, pi, int(di), ns, po, int(do)))
         return out
+
+    def set_coarse_mode(self, mode: int, bands: int = 0):
+        """0: owner-G chain; 1: space-parallel G over P row bands (P = nranks, or `bands`
+        virtual bands on one rank)."""
+        self._check(self.L.prs_set_coarse_mode(self.h, mode, bands))
 
     def set_profiling(self, on: bool):
         self._check(self.L.prs_set_profiling(self.h, int(on)))

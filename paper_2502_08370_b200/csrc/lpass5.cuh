@@ -37,6 +37,8 @@ struct L5Args {
     int order;            // tile order: 0 column block fastest; 1 state fastest (pivot tiles
                           // shared by all states are then read by co-resident CTAs: L2 hits)
     int s8, nsg8;         // lpass8: slices per CTA, slice groups
+    int row0;             // global row of local row 0 (a band of the lines, space-parallel G)
+    const double *ybeg, *xend;  // lp5_scan: y entering / x leaving each line (per line; NULL: 0)
     double tau, h2inv;
     CoefTab tab;
     const double *invd, *s2n, *s2f;
@@ -105,8 +107,9 @@ template <int COEF>
 __device__ __forceinline__ void l5_load(const L5Args &a, const L5Tile &T, int w, int t, L5Chunk<COEF> &c) {
     const int n = a.n;
     const int col = T.cb * L5W + w;
-    const int r0 = T.rb * L5RB + t * LCH;
-    const double *src = a.in + T.base + (long long)r0 * a.Sl + col;
+    const int lr0 = T.rb * L5RB + t * LCH;  // local row (in the state / band)
+    const int r0 = a.row0 + lr0;             // global row (coefficients, line boundary)
+    const double *src = a.in + T.base + (long long)lr0 * a.Sl + col;
 #pragma unroll
     for (int i = 0; i < LCH; ++i) c.v[i] = src[(long long)i * a.Sl];
     c.tauh = a.tau * a.h2inv;
@@ -164,13 +167,13 @@ __global__ void lp5_scan_kernel(L5Args a, long long ncols) {
     const long long sq = idx / a.n;
     const int col = (int)(idx - sq * a.n);
     const long long o0 = sq * a.nrb * a.n + col;
-    double Y = 0.0;
+    double Y = a.ybeg ? a.ybeg[idx] : 0.0;  // y entering the first block (0 at the line start)
     for (int rb = 0; rb < a.nrb; ++rb) {
         const long long o = o0 + (long long)rb * a.n;
         a.yx[o] = Y;
         Y = fma(a.tt[o], Y, a.tt[a.tstride + o]);
     }
-    double X = 0.0;  // x after the last block
+    double X = a.xend ? a.xend[idx] : 0.0;  // x after the last block (0 at the line end)
     for (int rb = a.nrb - 1; rb >= 0; --rb) {
         const long long o = o0 + (long long)rb * a.n;
         a.yx[a.tstride + o] = X;
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(L5T, 2) lp5_finish_kernel(L5Args a) {
     }
     // ---- store + fused epilogue ----
     const int col = T.cb * L5W + w;
-    const long long g0 = T.base + (long long)(T.rb * L5RB + t * LCH) * a.Sl + col;
+    const long long g0 = T.base + (long long)(T.rb * L5RB + t * LCH) * a.Sl + col;  // local rows
     double dmax = 0.0;
     unsigned long long bad = 0;
 #pragma unroll

@@ -27,6 +27,7 @@
 #include "lpass8.cuh"
 #include "lpass9.cuh"
 #include "xy3.cuh"
+#include "gpar.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -45,6 +46,9 @@ struct Nccl {
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
     bool load(std::string &err) {
         if (h) return true;
@@ -65,6 +69,9 @@ struct Nccl {
         SYM(Send, "ncclSend");
         SYM(Recv, "ncclRecv");
         SYM(AllReduce, "ncclAllReduce");
+        SYM(AllGather, "ncclAllGather");
+        SYM(GroupStart, "ncclGroupStart");
+        SYM(GroupEnd, "ncclGroupEnd");
         SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
         return true;
@@ -139,6 +146,14 @@ struct prs_ctx {
     // >= 2^18 points (PRS_SKIP=0/1 overrides); bare fine_sweep / correct calls never skip.
     bool skip_converged = false;
     int kconv = 0;
+    // space-parallel G (gpar.cuh): P bands of gnb rows; one process runs all P (virtual bands)
+    int gpar = 0, gP = 1, gnb = 0;
+    double *gb_u = nullptr, *gb_d = nullptr, *gb_gc = nullptr;  // multi-rank: this rank's band of
+                                                                 // U_0..U_N, Delta_0.., Gcache_0..
+    double *gb_v = nullptr;    // x-stage output (a full state: P bands when virtual)
+    double *gb_tt = nullptr;   // per band: block tuples [5] + scan [2] x (gnb/64) x n
+    double *gb_tot = nullptr;  // band tuples [P][5][n]
+    double *gb_yx = nullptr;   // per band: y entering / x leaving [P][2][n]
     double *l5buf = nullptr;  // lpass5 block tuples and block y/x
     size_t l5_bytes = 0;
     std::string err;
@@ -1167,6 +1182,11 @@ void prs_destroy(prs_ctx *ctx) {
     if (ctx->l5buf) cudaFree(ctx->l5buf);
     if (ctx->l9buf) cudaFree(ctx->l9buf);
     if (ctx->fine_exec) cudaGraphExecDestroy(ctx->fine_exec);
+    {
+        double *gb[] = {ctx->gb_u, ctx->gb_d, ctx->gb_gc, ctx->gb_v, ctx->gb_tt, ctx->gb_tot, ctx->gb_yx};
+        for (double *b : gb)
+            if (b) cudaFree(b);
+    }
     if (ctx->corr_exec) cudaGraphExecDestroy(ctx->corr_exec);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1302,6 +1322,196 @@ int prs_fine_sweep(prs_ctx *ctx) {
     return PRS_OK;
 }
 
+// ---------------------------------------------------------- space-parallel G -------
+static L5Args gp_l5(prs_ctx *ctx, int b) {
+    const int n = ctx->p.n, nrb = ctx->gnb / L5RB;
+    const TauFactors &f = ctx->fac[0];
+    L5Args a{};
+    a.vol = (long long)ctx->gnb * n;
+    a.n = n;
+    a.Sl = n;
+    a.nq = 1;
+    a.Sq = a.vol;
+    a.nrb = nrb;
+    a.ncb = n / L5W;
+    a.nsq = 1;
+    a.ntiles = (long long)nrb * a.ncb;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    a.invd = f.invdy;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    a.tstride = (long long)nrb * n;
+    a.tt = ctx->gb_tt + (long long)b * 7 * a.tstride;
+    a.yx = a.tt + 5 * a.tstride;
+    a.row0 = b * ctx->gnb;
+    a.ybeg = ctx->gb_yx + (long long)b * 2 * n;
+    a.xend = a.ybeg + n;
+    a.e_red = ctx->red;
+    return a;
+}
+
+// phase 1 of band b's G step for slice `slice`: x stage (row-local) into v, the band's y block
+// tuples and its band tuple (gb_tot[b])
+static int gp_phase1(prs_ctx *ctx, int b, const double *in, double *v, int slice) {
+    const int n = ctx->p.n;
+    const TauFactors &f = ctx->fac[0];
+    X3Args x{};
+    x.in = in;
+    x.out = v;
+    x.vol = (long long)ctx->gnb * n;
+    x.n = n;
+    x.P = n / LCH;
+    x.lines_per_state = ctx->gnb;
+    x.ngroups = (long long)ctx->gnb * n / 4096;
+    x.nstates = 1;
+    x.nranges = 0;
+    x.dim = 2;
+    x.row0 = b * ctx->gnb;
+    x.tau = f.tau;
+    x.h2inv = ctx->h2inv;
+    x.creact = ctx->creact;
+    x.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
+    x.sinpi = ctx->sinpi;
+    x.ta = coarse_time(ctx, slice);
+    x.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
+    x.invd = f.invdx;
+    x.s2n = ctx->s2n;
+    x.s2f = ctx->s2f;
+    const int coef = ctx->p.coef_kind, src = ctx->p.source_kind;
+    void (*kx)(X3Args) = nullptr;
+#define XK(C, S_) if (coef == C && src == S_) kx = xpass3_kernel<C, 0, S_>;
+    XK(0, 0) XK(0, 1) XK(1, 0) XK(1, 1)
+#undef XK
+    const size_t shm = xpass3_smem_bytes(coef);
+    CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    kx<<<(unsigned)std::min<long long>(ctx->num_sms, x.ngroups), X3T, shm, ctx->stream>>>(x);
+    TRY(last_launch(ctx));
+    L5Args a = gp_l5(ctx, b);
+    a.in = v;
+    a.out = v;
+    (coef ? lp5_tuples_kernel<1> : lp5_tuples_kernel<0>)<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    gp_band_total_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(a, ctx->gb_tot + (long long)b * 5 * n);
+    TRY(last_launch(ctx));
+    return PRS_OK;
+}
+
+// phase 2 of band b: boundary values from all band tuples, scan, finish with the fused
+// correction epilogue on the band's rows of U_{n+1}, the G cache and Delta_n
+static int gp_phase2(prs_ctx *ctx, int b, double *v, double *traj_next, double *gcache, const double *delta) {
+    const int n = ctx->p.n;
+    L5Args a = gp_l5(ctx, b);
+    a.in = v;
+    a.out = v;
+    a.e_traj = traj_next;
+    a.e_gcache = gcache;
+    a.e_delta = delta;
+    gp_boundary_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->gb_tot, ctx->gP, b, n,
+                                                                 const_cast<double *>(a.ybeg),
+                                                                 const_cast<double *>(a.xend));
+    TRY(last_launch(ctx));
+    lp5_scan_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(a, (long long)n);
+    TRY(last_launch(ctx));
+    (ctx->p.coef_kind ? lp5_finish_kernel<1, EPI_CORRECT> : lp5_finish_kernel<0, EPI_CORRECT>)
+        <<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
+    TRY(last_launch(ctx));
+    return PRS_OK;
+}
+
+// the correction chain with space-parallel G.  One process: every slice, all P bands are
+// views into the full states.  P ranks: this rank's band of every state, Delta bands
+// scattered from the slice owners first, U / G-cache bands gathered back afterwards.
+static int gp_correct(prs_ctx *ctx) {
+    const int n = ctx->p.n, P = ctx->gP;
+    const long long bvol = (long long)ctx->gnb * n;
+    const size_t bbytes = sizeof(double) * (size_t)bvol;
+    CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
+    if (ctx->nranks == 1) {
+        for (int i = local_start(ctx); i < ctx->count; ++i) {
+            for (int b = 0; b < P; ++b)
+                TRY(gp_phase1(ctx, b, state(ctx, ctx->traj, i) + b * bvol, ctx->gb_v + b * bvol, ctx->first + i));
+            for (int b = 0; b < P; ++b)
+                TRY(gp_phase2(ctx, b, ctx->gb_v + b * bvol, state(ctx, ctx->traj, i + 1) + b * bvol,
+                              state(ctx, ctx->gcache, i) + b * bvol, state(ctx, ctx->delta, i) + b * bvol));
+        }
+        return PRS_OK;
+    }
+    const int me = ctx->rank, N = ctx->p.N;
+    // U_0's band (U^{k+1}_0 = U_0)
+    CK(cudaMemcpyAsync(ctx->gb_u, ctx->u0 + (long long)me * bvol, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    auto owner = [&](int slice) {
+        for (int q = 0; q < ctx->nranks; ++q) {
+            int f0 = 0, c0 = 0;
+            prs_partition(N, ctx->nranks, q, &f0, &c0);
+            if (slice >= f0 && slice < f0 + c0) return q;
+        }
+        return -1;
+    };
+    // scatter: band p of Delta_n from owner(n) to rank p
+    NK(g_nccl.GroupStart());
+    for (int sl = 0; sl < N; ++sl) {
+        const int q = owner(sl);
+        if (q == me) {
+            const double *d = state(ctx, ctx->delta, sl - ctx->first);
+            for (int p = 0; p < P; ++p) {
+                if (p == me)
+                    CK(cudaMemcpyAsync(ctx->gb_d + sl * bvol, d + p * bvol, bbytes, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+                else
+                    NK(g_nccl.Send(d + p * bvol, (size_t)bvol, ncclDouble, p, ctx->comm, ctx->stream));
+            }
+        } else {
+            NK(g_nccl.Recv(ctx->gb_d + sl * bvol, (size_t)bvol, ncclDouble, q, ctx->comm, ctx->stream));
+        }
+    }
+    NK(g_nccl.GroupEnd());
+    // the chain on this rank's band: exchange the band tuples after phase 1 of every step
+    for (int sl = 0; sl < N; ++sl) {
+        TRY(gp_phase1(ctx, me, ctx->gb_u + sl * bvol, ctx->gb_v, sl));
+        NK(g_nccl.AllGather(ctx->gb_tot + (long long)me * 5 * n, ctx->gb_tot, (size_t)5 * n, ncclDouble, ctx->comm,
+                            ctx->stream));
+        TRY(gp_phase2(ctx, me, ctx->gb_v, ctx->gb_u + (sl + 1) * bvol, ctx->gb_gc + sl * bvol,
+                      ctx->gb_d + sl * bvol));
+    }
+    // gather: U_{n+1} and Gcache_n bands to the owner of slice n, and U_first to this rank
+    NK(g_nccl.GroupStart());
+    for (int sl = 0; sl < N; ++sl) {
+        const int q = owner(sl);
+        const int qn = (sl + 1 < N) ? owner(sl + 1) : -1;  // U_{sl+1} is also the next owner's input
+        for (int p = 0; p < P; ++p) {
+            // U_{sl+1}: band p -> owner(sl) (end state) and, at a rank edge, -> owner(sl+1)
+            for (int dst : {q, (qn != q) ? qn : -1}) {
+                if (dst < 0) continue;
+                if (p == me && dst == me) {
+                    double *t = (dst == q) ? state(ctx, ctx->traj, sl + 1 - ctx->first) : ctx->traj;
+                    CK(cudaMemcpyAsync(t + p * bvol, ctx->gb_u + (sl + 1) * bvol, bbytes, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+                } else if (p == me) {
+                    NK(g_nccl.Send(ctx->gb_u + (sl + 1) * bvol, (size_t)bvol, ncclDouble, dst, ctx->comm,
+                                   ctx->stream));
+                } else if (dst == me) {
+                    double *t = (dst == q) ? state(ctx, ctx->traj, sl + 1 - ctx->first) : ctx->traj;
+                    NK(g_nccl.Recv(t + p * bvol, (size_t)bvol, ncclDouble, p, ctx->comm, ctx->stream));
+                }
+            }
+            // Gcache_sl: band p -> owner(sl)
+            if (p == me && q == me) {
+                CK(cudaMemcpyAsync(state(ctx, ctx->gcache, sl - ctx->first) + p * bvol, ctx->gb_gc + sl * bvol,
+                                   bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+            } else if (p == me) {
+                NK(g_nccl.Send(ctx->gb_gc + sl * bvol, (size_t)bvol, ncclDouble, q, ctx->comm, ctx->stream));
+            } else if (q == me) {
+                NK(g_nccl.Recv(state(ctx, ctx->gcache, sl - ctx->first) + p * bvol, (size_t)bvol, ncclDouble, p,
+                               ctx->comm, ctx->stream));
+            }
+        }
+    }
+    NK(g_nccl.GroupEnd());
+    return PRS_OK;
+}
+
 // the local part of the coarse correction chain: G step + fused correction
 // epilogue for every local slice, in time order
 static int enqueue_correct_chain(prs_ctx *ctx) {
@@ -1321,7 +1531,11 @@ static int enqueue_correct_chain(prs_ctx *ctx) {
 int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
     if (!ctx) return PRS_EINVAL;
     if (!ctx->delta) { ctx->err = "prs_fine_sweep first"; return PRS_EINVAL; }
-    if (ctx->nranks > 1) {
+    if (ctx->gpar) {
+        TRY(gp_correct(ctx));
+        if (ctx->nranks > 1)
+            NK(g_nccl.AllReduce(ctx->red, ctx->red, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    } else if (ctx->nranks > 1) {
         CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
         if (ctx->rank > 0)
             NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
@@ -1334,14 +1548,12 @@ int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
             TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
                          coarse_time(ctx, ctx->first + i), ep, false, ctx->ss));
         }
-    } else {
-        TRY(run_graphed(ctx, enqueue_correct_chain, ctx->corr_calls, ctx->corr_exec, ctx->corr_glaunch));
-    }
-    if (ctx->nranks > 1) {
         if (ctx->rank < ctx->nranks - 1)
             NK(g_nccl.Send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ncclDouble, ctx->rank + 1,
                            ctx->comm, ctx->stream));
         NK(g_nccl.AllReduce(ctx->red, ctx->red, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    } else {
+        TRY(run_graphed(ctx, enqueue_correct_chain, ctx->corr_calls, ctx->corr_exec, ctx->corr_glaunch));
     }
     CK(cudaMemcpyAsync(ctx->red_host, ctx->red, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -1446,6 +1658,50 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
     CK(cudaMemcpyAsync(out, buf[cur], ctx->sbytes, out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    return PRS_OK;
+}
+
+int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands) {
+    if (!ctx || (mode != 0 && mode != 1)) return PRS_EINVAL;
+    if (mode == 0) {
+        ctx->gpar = 0;
+        return PRS_OK;
+    }
+    const int n = ctx->p.n;
+    const int P = (ctx->nranks > 1) ? ctx->nranks : bands;
+    const bool pow2 = P >= 1 && (P & (P - 1)) == 0 && (n & (n - 1)) == 0;
+    if (ctx->p.dim != 2 || ctx->p.split != 0 || ctx->p.G != PRS_FIE || !pow2 || n > 4096 || n % (L5RB * P) != 0 ||
+        (long long)n * n / P < 4096) {
+        ctx->err = "space-parallel G: 2-D dimensional split, G = FIE, P a power of two, n a power of two "
+                   "<= 4096 with n % (64 P) == 0";
+        return PRS_EUNSUPPORTED;
+    }
+    if (ctx->nranks > 1 && bands != ctx->nranks && bands != 0) {
+        ctx->err = "space-parallel G over ranks: one band per rank";
+        return PRS_EINVAL;
+    }
+    ctx->gP = P;
+    ctx->gnb = n / P;
+    const long long bvol = (long long)ctx->gnb * n, nrb = ctx->gnb / L5RB;
+    double **bufs[] = {&ctx->gb_u, &ctx->gb_d, &ctx->gb_gc, &ctx->gb_v, &ctx->gb_tt, &ctx->gb_tot, &ctx->gb_yx};
+    for (double **b : bufs)
+        if (*b) {
+            CK(cudaFree(*b));
+            *b = nullptr;
+        }
+    if (ctx->nranks > 1) {
+        const int N = ctx->p.N;
+        CK(cudaMalloc(&ctx->gb_u, sizeof(double) * bvol * (N + 1)));
+        CK(cudaMalloc(&ctx->gb_d, sizeof(double) * bvol * N));
+        CK(cudaMalloc(&ctx->gb_gc, sizeof(double) * bvol * N));
+        CK(cudaMalloc(&ctx->gb_v, sizeof(double) * bvol));
+    } else {
+        CK(cudaMalloc(&ctx->gb_v, sizeof(double) * bvol * P));
+    }
+    CK(cudaMalloc(&ctx->gb_tt, sizeof(double) * 7 * nrb * n * P));
+    CK(cudaMalloc(&ctx->gb_tot, sizeof(double) * 5 * (size_t)n * P));
+    CK(cudaMalloc(&ctx->gb_yx, sizeof(double) * 2 * (size_t)n * P));
+    ctx->gpar = 1;
     return PRS_OK;
 }
 

@@ -37,6 +37,8 @@ struct X3Args {
                           // the per-point pivot rows they share hit L2; 0: one contiguous range
                           // of the whole batch per CTA
     int dim;
+    int row0;             // 2-D: global row of the state's first line (a band of a state, SURVEY
+                          // 8(e) space-parallel G); 0 for whole states
     double tau, h2inv, creact;
     double src_amp;
     const double *sinpi;
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
     // pivot rows repeat every state: the group of pivots for global group g starts at
     // row (g * lpg) mod lines_per_state
     auto issue_piv = [&](long long g) {
-        const long long row0 = (g * lpg) & (a.lines_per_state - 1);
+        const long long row0 = ((g * lpg) & (a.lines_per_state - 1)) + a.row0;
         issue_group(a.invd + row0 * n - 0, 0, ib(g));
     };
 
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         if (gg >= G) return s;
         const long long gl = gg * lpg + l;
         const long long bs = gl >> lps_sh;
-        const int jj = (int)(gl & (a.lines_per_state - 1));
+        const int jj = (int)(gl & (a.lines_per_state - 1)) + a.row0;
         if (DR && COEF) {
             s.kfm = __ldg(a.s2f + jj);
             s.kfp = __ldg(a.s2f + jj + 1);

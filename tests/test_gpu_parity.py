@@ -552,3 +552,48 @@ def test_iterate_skipping_converged_slices_is_bitwise_neutral(p, monkeypatch):
     if fine is not None:
         scale = max(float(np.max(np.abs(t))) for t in fine)
         assert float(np.max(np.abs(outs[0][2] - fine))) / scale <= TOL
+
+
+@pytest.mark.parametrize("p,bands", [
+    (Problem(dim=2, n=256, c=1.0, coef=1, N=4, s=3, G=FIE, F=DR, init="modes", seed=2), 4),
+    (Problem(dim=2, n=256, c=1.0, coef=1, N=5, s=2, G=FIE, F=FIE, init="modes", seed=3), 2),
+    (Problem(dim=2, n=128, c=1.0, source=1, N=4, s=4, G=FIE, F=FIE), 2),
+    (Problem(dim=2, n=1024, c=1.0, coef=1, N=3, s=2, G=FIE, F=DR, init="modes", seed=4), 8),
+], ids=lambda x: x.label() if hasattr(x, "label") else f"P{x}")
+def test_space_parallel_g_virtual_bands_match_oracle(p, bands):
+    """SURVEY 8(e) space-parallel G: the coarse chain on P row bands (partitioned tridiagonal
+    y stage through all-gathered band tuples), here P virtual bands in one process, matches
+    the oracle at every iteration (and owner-G up to rounding)."""
+    prs = prs_mod()
+    u0 = synth.initial_state(p)
+    o = oracle.Oracle(p)
+    ctrajs, cupds = o.parareal(u0, p.N, fixed=True)
+    ctx = prs.Context(p)
+    ctx.set_coarse_mode(1, bands)
+    ctx.set_initial(dev(u0))
+    ctx.coarse_sweep()
+    buf = torch.empty((p.n, p.n), dtype=torch.float64, device="cuda")
+    for k in range(p.N + 1):
+        got = np.stack([host(ctx.get_slice(n, buf)).copy() for n in range(p.N + 1)])
+        scale = max(float(np.max(np.abs(u0))), float(np.max(np.abs(ctrajs[k]))))
+        assert float(np.max(np.abs(got - ctrajs[k]))) / scale <= TOL, k
+        if k < p.N:
+            ctx.fine_sweep()
+            upd = ctx.parareal_correct()
+            assert abs(upd - cupds[k]) <= TOL * max(1.0, cupds[k]), (k, upd, cupds[k])
+    ctx.close()
+
+
+def test_space_parallel_g_rejects_unsupported_shapes():
+    prs = prs_mod()
+    ctx = prs.Context(Problem(dim=2, n=256, N=4, s=2, G=DR, F=DR))
+    with pytest.raises(prs.PrsError) as ei:
+        ctx.set_coarse_mode(1, 2)
+    assert ei.value.code == prs.PRS_EUNSUPPORTED
+    ctx.close()
+    ctx = prs.Context(Problem(dim=2, n=256, N=4, s=2, G=FIE, F=DR))
+    with pytest.raises(prs.PrsError):
+        ctx.set_coarse_mode(1, 8)  # 256 rows cannot form 8 bands of >= 64 rows
+    ctx.set_coarse_mode(1, 4)
+    ctx.set_coarse_mode(0)
+    ctx.close()
