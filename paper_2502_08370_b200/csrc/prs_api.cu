@@ -28,6 +28,7 @@
 #include "lpass9.cuh"
 #include "xy3.cuh"
 #include "gpar.cuh"
+#include "sweep2.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -129,6 +130,7 @@ struct prs_ctx {
     bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
     bool x3_contig = false;    // PRS_X3CONTIG=1: xpass3 takes one contiguous range per CTA
+    bool no_sweep2 = false;    // PRS_SWEEP2=0: small 2-D slices step through the per-step kernels
     bool no_tiled = true;      // PRS_TILED=1: 2-D long lines take lp9 x tiles + lp8 (opt-in:
                                // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
     double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
@@ -1075,6 +1077,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *swv = getenv("PRS_SWEEP2");
+        ctx->no_sweep2 = swv && swv[0] == '0';
         const char *x3c = getenv("PRS_X3CONTIG");
         ctx->x3_contig = x3c && x3c[0] == '1';
         const char *xyv = getenv("PRS_XY");
@@ -1250,11 +1254,73 @@ static int local_start(const prs_ctx *ctx) {
     return k <= 0 ? 0 : (k > ctx->count ? ctx->count : k);
 }
 
+// small 2-D slices (kappa = 1, n = 32 / 64 / 128 / 256): the whole sweep on chip (sweep2.cuh)
+static bool sweep2_ok(const prs_ctx *ctx) {
+    const int n = ctx->p.n;
+    return !ctx->no_sweep2 && !ctx->force_v2 && ctx->p.dim == 2 && ctx->p.split == 0 && ctx->p.coef_kind == 0 &&
+           (n == 32 || n == 64 || n == 128 || n == 256);
+}
+
+static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const double *gc, long long B, long long slice0) {
+    const int n = ctx->p.n;
+    const TauFactors &f = ctx->fac[1];
+    SWArgs a{};
+    a.in = in;
+    a.out = out;
+    a.gc = gc;
+    a.vol = ctx->ss;
+    a.s = ctx->p.s;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.creact = ctx->creact;
+    a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
+    a.sinpi = ctx->sinpi;
+    a.slice0 = slice0;
+    a.dt = ctx->dt;
+    a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
+    const int dr = (ctx->p.F == PRS_DR) ? 1 : 0, src = ctx->p.source_kind, epi = gc ? EPI_DELTA : EPI_STORE;
+    void (*k)(SWArgs) = nullptr;
+    size_t shm = 0;
+#define SK(N_, D, S_, E)                                                   \
+    if (n == N_ && dr == D && src == S_ && epi == E) {                     \
+        k = sweep2_kernel<N_, D, S_, E>;                                   \
+        shm = sizeof(double) * sweep2_smem_doubles<N_>();                   \
+    }
+#define SKN(N_) SK(N_, 0, 0, 0) SK(N_, 0, 1, 0) SK(N_, 1, 0, 0) SK(N_, 1, 1, 0) \
+                SK(N_, 0, 0, 1) SK(N_, 0, 1, 1) SK(N_, 1, 0, 1) SK(N_, 1, 1, 1)
+    SKN(32) SKN(64) SKN(128) SKN(256)
+#undef SKN
+#undef SK
+    const int CL = n / SW_R;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(B * CL));
+    cfg.blockDim = dim3(SW_T);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (ctx->prof) TRY(prof_begin(ctx));
+    CK(cudaLaunchKernelEx(&cfg, k, a));
+    TRY(last_launch(ctx));
+    // 32 B per update for a 2-D step; on chip here, so the rate is an effective one
+    if (ctx->prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * ctx->p.s * 32.0));
+    return PRS_OK;
+}
+
 static int enqueue_fine_sweep(prs_ctx *ctx) {
     const int s = ctx->p.s;
     const int i0 = local_start(ctx);
     const long long B = ctx->count - i0;
     if (B <= 0) return PRS_OK;
+    if (sweep2_ok(ctx))
+        return launch_sweep2(ctx, state(ctx, ctx->traj, i0), state(ctx, (s & 1) ? ctx->fa : ctx->fb, i0),
+                             state(ctx, ctx->gcache, i0), B, ctx->first + i0);
     const double *src = state(ctx, ctx->traj, i0);
     double *bufs[2] = {state(ctx, ctx->fa, i0), state(ctx, ctx->fb, i0)};
     for (int j = 0; j < s; ++j) {

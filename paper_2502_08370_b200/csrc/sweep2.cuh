@@ -1,0 +1,295 @@
+// sweep2.cuh -- the whole fine sweep F^s of a small 2-D slice on chip (kappa = 1,
+// n = 32 CL with CL = 1, 2, 4, 8 CTAs per cluster; c0: n = 32, c1 / c1p: n = 256).
+//
+// F^s is s FIE or DR steps of delta t.  For small states the per-step kernels
+// are latency-bound (c1: 36 us per step for 32 slices of 512 KB, L2-resident).  Here one cluster
+// of CL CTAs holds one slice for all s steps: each CTA keeps 32 rows in shared memory, so the
+// state is read once at the start and Delta_n = F^s(U) - G(U) written once at the end.
+// Per step (PAPER.md:153-157 FIE, 167-171 DR in the M = 2 form of DESIGN.md R1):
+//  * x stage: rows are CTA-local; r_1 = U (+ tau A_y U for DR, rows j +- 1 of the neighbour
+//    CTAs read through distributed shared memory) (+ tau F); chunk-parallel Thomas with
+//    segmented warp scans over the CH = n/16 chunks of a row; r_2 = V_1 (- w) in place;
+//  * y stage: columns cross the cluster: each thread walks 16-row chunks (lpass4.cuh 5-tuples),
+//    the CTA totals per column are exchanged through distributed shared memory (every CTA
+//    composes the totals of the CTAs before and after it), then the exact recurrences.
+// Pivot tables (kappa = 1: the same for x and y) sit chunk-padded in shared memory.
+#pragma once
+#include "common.cuh"
+#include "lpass.cuh"
+#include "lpass4.cuh"
+
+namespace prs {
+
+constexpr int SW_R = 32;   // rows per CTA
+constexpr int SW_T = 256;  // threads per CTA
+
+struct SWArgs {
+    const double *in;     // U^k_n of the batch (slice stride vol)
+    double *out;          // Delta_n (EPI_DELTA) or F^s(U) (EPI_STORE)
+    const double *gc;     // G cache (EPI_DELTA)
+    long long vol;
+    int s;                // fine steps
+    double tau, h2inv, creact, src_amp;
+    const double *sinpi;
+    long long slice0;     // global slice index of batch state 0
+    double dt;
+    CoefTab tab;          // kappa = 1 pivots of (I - tau A_d), length n
+};
+
+// n = 256: each thread owns both 16-row chunks of its column, so the chunk tuples and the
+// per-column boundary values stay in registers (no chk / yxb buffers: 2 CTAs per SM fit)
+template <int N>
+constexpr bool sweep2_own_column() { return N == SW_T; }
+template <int N>
+constexpr size_t sweep2_smem_doubles() {
+    return (size_t)SW_R * (N + N / LCH) + 3 * (N + N / LCH) + (sweep2_own_column<N>() ? 0 : 5 * 2 * N + 2 * N) +
+           5 * N + 2 * 2 * (N + N / LCH);
+}
+
+template <int N, int DR, int SRC, int EPI>
+__global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
+    constexpr int CL = N / SW_R;      // CTAs per slice
+    constexpr int S = N + N / LCH;    // padded row stride
+    constexpr int CH = N / LCH;       // chunks per row
+    constexpr int XT = SW_R * CH;     // x tasks (row, chunk)
+    constexpr int YT = 2 * N;         // y tasks (column, chunk of 16 rows)
+    extern __shared__ __align__(16) double sm[];
+    double *tile = sm;                          // 32 x S
+    double *tb = tile + SW_R * S;               // [3][S] m, id, cc (chunk-padded)
+    constexpr bool OWN = sweep2_own_column<N>();
+    double *ctot = tb + 3 * S;                  // [5][N] this CTA's column totals (read remotely)
+    double *edge = ctot + 5 * N;                // [parity][2][S] copies of the first / last row (DR halo
+                                                // for the neighbours, published at the end of each step)
+    double *chk = edge + 2 * 2 * S;             // (!OWN) [5][2][N] chunk tuples (y)
+    double *yxb = chk + 5 * 2 * N;              // (!OWN) [2][N] y entering / x leaving this CTA
+    cg::cluster_group cl = cg::this_cluster();
+    const int crank = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31;
+    const long long b = blockIdx.x / CL;
+    const int r0 = crank * SW_R;  // first global row of this CTA
+    const long long base = b * a.vol + (long long)r0 * N;
+
+    for (int e = tid; e < N; e += SW_T) {
+        tb[cpad(e)] = __ldg(a.tab.m + e);
+        tb[S + cpad(e)] = __ldg(a.tab.id + e);
+        tb[2 * S + cpad(e)] = __ldg(a.tab.cc + e);
+    }
+    for (int e = tid; e < SW_R * N / 2; e += SW_T) {
+        const int r = e / (N / 2), x2 = (e % (N / 2)) * 2;
+        const double2 v = __ldg(reinterpret_cast<const double2 *>(a.in + base + (long long)r * N + x2));
+        double *d = tile + r * S + cpad(x2);
+        d[0] = v.x;
+        d[1] = v.y;
+    }
+    // neighbour CTAs' published edge rows (DR halo rows)
+    const double *edge_up = (crank > 0) ? cl.map_shared_rank(edge, crank - 1) : nullptr;
+    const double *edge_dn = (crank < CL - 1) ? cl.map_shared_rank(edge, crank + 1) : nullptr;
+    auto publish_edges = [&](int par) {  // rows 0 and 31 of the tile -> edge[par]
+        double *e = edge + par * 2 * S;
+        for (int x = tid; x < S; x += SW_T) {
+            e[x] = tile[x];
+            e[S + x] = tile[(SW_R - 1) * S + x];
+        }
+    };
+    if (DR) {
+        __syncthreads();  // the whole tile is loaded
+        publish_edges(0);
+    }
+    const double tauh = a.tau * a.h2inv, taucr = a.tau * a.creact;
+    constexpr int NXT = (XT + SW_T - 1) / SW_T, NYT = (YT + SW_T - 1) / SW_T;
+
+    for (int j = 0; j < a.s; ++j) {
+        cl.sync();  // previous step complete in every CTA (edge rows published, remote totals consumed)
+        const int par = j & 1;
+        // ---------------- x stage ----------------
+        // (a) w = tau A_y U of every task (reads rows r-1, r+1, the neighbour CTAs' edge rows)
+        double w[NXT][LCH];
+#pragma unroll
+        for (int k = 0; k < NXT; ++k) {
+            const int q = tid + k * SW_T;
+            if (!DR || q >= XT) break;
+            const int r = q / CH, c = q % CH;
+            const double *p = tile + r * S + c * LCP;
+            // the neighbours' edge rows come from their published copies (parity of this step),
+            // so the in-place solve below needs no cluster barrier before it
+            const double *pm = (r > 0) ? p - S : (edge_up ? edge_up + par * 2 * S + S + c * LCP : nullptr);
+            const double *pp = (r < SW_R - 1) ? p + S : (edge_dn ? edge_dn + par * 2 * S + c * LCP : nullptr);
+#pragma unroll
+            for (int i = 0; i < LCH; ++i) {
+                const double uu = p[i];
+                const double dm = pm ? pm[i] : 0.0, dp = pp ? pp[i] : 0.0;
+                w[k][i] = fma(tauh, (dp - uu) - (uu - dm), -taucr * uu);
+            }
+        }
+        if (DR) __syncthreads();  // every read of other tasks' rows of this tile is done
+        // (b) r_1 = U (+ w) (+ tau F) from the task's own region (untouched so far), solve, r_2 back
+#pragma unroll
+        for (int k = 0; k < NXT; ++k) {
+            const int q = tid + k * SW_T;
+            if (q >= XT) break;  // (uniform per warp: XT is a multiple of 32)
+            const int r = q / CH, c = q % CH, tl = lane % CH;
+            double *p = tile + r * S + c * LCP;
+            double v[LCH];
+#pragma unroll
+            for (int i = 0; i < LCH; ++i) v[i] = DR ? p[i] + w[k][i] : p[i];
+            if (SRC) {
+                const double t = (double)((a.slice0 + b) * a.s + j + 1) * a.dt;
+                const double f = a.tau * a.src_amp * exp(-t) * __ldg(a.sinpi + r0 + r);
+#pragma unroll
+                for (int i = 0; i < LCH; ++i) v[i] = fma(f, __ldg(a.sinpi + c * LCH + i), v[i]);
+            }
+            const double *tm = tb + c * LCP, *ti = tb + S + c * LCP, *tc = tb + 2 * S + c * LCP;
+            double A = 1.0, B = 0.0;
+#pragma unroll
+            for (int i = 0; i < LCH; ++i) {
+                B = fma(-tm[i], B, v[i]);
+                A = -tm[i] * A;
+            }
+            double EA, EB;
+            seg_scan_fwd(A, B, CH, tl, EA, EB);
+            double y = EB, Pb = 1.0, Qb = 0.0;
+#pragma unroll
+            for (int i = 0; i < LCH; ++i) {
+                y = fma(-tm[i], y, v[i]);
+                v[i] = y;
+                Qb = fma(Pb * ti[i], y, Qb);
+                Pb *= -tc[i];
+            }
+            double EP, EQ;
+            seg_scan_bwd(Pb, Qb, CH, tl, EP, EQ);
+            double x = EQ;
+#pragma unroll
+            for (int i = LCH - 1; i >= 0; --i) {
+                x = fma(ti[i], v[i], -tc[i] * x);
+                p[i] = DR ? x - w[k][i] : x;
+            }
+        }
+        __syncthreads();
+        // ---------------- y stage ----------------
+        Tup tu[NYT];
+        auto ym = [&](int t, int i) { return tb[cpad(r0 + t * LCH) + i]; };
+        auto yi = [&](int t, int i) { return tb[S + cpad(r0 + t * LCH) + i]; };
+        auto yc = [&](int t, int i) { return tb[2 * S + cpad(r0 + t * LCH) + i]; };
+#pragma unroll
+        for (int k = 0; k < NYT; ++k) {
+            const int q = tid + k * SW_T;
+            if (q >= YT) break;
+            const int col = q % N, t = q / N;
+            const double *p = tile + (t * LCH) * S + cpad(col);
+            double y0 = 0.0, g = 1.0, cp = 1.0, Q = 0.0, R = 0.0;
+#pragma unroll
+            for (int i = 0; i < LCH; ++i) {
+                const double m = ym(t, i);
+                y0 = fma(-m, y0, p[i * S]);
+                g = -m * g;
+                const double cid = cp * yi(t, i);
+                Q = fma(cid, y0, Q);
+                R = fma(cid, g, R);
+                cp *= -yc(t, i);
+            }
+            tu[k] = Tup{g, y0, cp, Q, R};
+            if (!OWN) {
+                chk[(0 * 2 + t) * N + col] = g;
+                chk[(1 * 2 + t) * N + col] = y0;
+                chk[(2 * 2 + t) * N + col] = cp;
+                chk[(3 * 2 + t) * N + col] = Q;
+                chk[(4 * 2 + t) * N + col] = R;
+            }
+        }
+        if (!OWN) __syncthreads();
+        auto getc = [&](int t, int col) {
+            return Tup{chk[(0 * 2 + t) * N + col], chk[(1 * 2 + t) * N + col], chk[(2 * 2 + t) * N + col],
+                       chk[(3 * 2 + t) * N + col], chk[(4 * 2 + t) * N + col]};
+        };
+        for (int col = tid; col < N; col += SW_T) {
+            const Tup tot = OWN ? tup_cat(tu[0], tu[1]) : tup_cat(getc(0, col), getc(1, col));
+            ctot[col] = tot.A;
+            ctot[N + col] = tot.B;
+            ctot[2 * N + col] = tot.P;
+            ctot[3 * N + col] = tot.Q;
+            ctot[4 * N + col] = tot.R;
+        }
+        cl.sync();  // every CTA's column totals visible
+        double Yown = 0.0, Xown = 0.0;  // (OWN) y entering / x leaving this CTA for column tid
+        for (int col = tid; col < N; col += SW_T) {
+            // y entering each CTA (compile-time indices only: the array stays in registers)
+            double yin[CL];
+            double Y = 0.0, Ymine = 0.0;
+#pragma unroll
+            for (int q = 0; q < CL; ++q) {
+                yin[q] = Y;
+                if (q == crank) Ymine = Y;
+                const double *ct = cl.map_shared_rank(ctot, q);
+                Y = fma(ct[col], Y, ct[N + col]);
+            }
+            double X = 0.0;
+#pragma unroll
+            for (int q = CL - 1; q >= 1; --q) {
+                if (q > crank) {
+                    const double *ct = cl.map_shared_rank(ctot, q);
+                    X = fma(ct[2 * N + col], X, fma(ct[4 * N + col], yin[q], ct[3 * N + col]));
+                }
+            }
+            if (OWN) {
+                Yown = Ymine;
+                Xown = X;
+            } else {
+                yxb[col] = Ymine;
+                yxb[N + col] = X;
+            }
+        }
+        if (!OWN) __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NYT; ++k) {
+            const int q = tid + k * SW_T;
+            if (q >= YT) break;
+            const int col = q % N, t = q / N;
+            double Y = OWN ? Yown : yxb[col];
+            if (t == 1) {
+                const Tup g0 = OWN ? tu[0] : getc(0, col);
+                Y = fma(g0.A, Y, g0.B);
+            }
+            const double Ylast = fma(tu[k].A, Y, tu[k].B);
+            double X = OWN ? Xown : yxb[N + col];
+            if (t == 0) {
+                const Tup g1 = OWN ? tu[NYT - 1] : getc(1, col);
+                X = fma(g1.P, X, fma(g1.R, Ylast, g1.Q));
+            }
+            // (the task's own column chunk is still r_2: re-read it, walk forward in place,
+            // then backward)
+            double *p = tile + (t * LCH) * S + cpad(col);
+            double y = Y;
+#pragma unroll
+            for (int i = 0; i < LCH; ++i) {
+                y = fma(-ym(t, i), y, p[i * S]);
+                p[i * S] = y;
+            }
+            double x = X;
+#pragma unroll
+            for (int i = LCH - 1; i >= 0; --i) {
+                x = fma(yi(t, i), p[i * S], -yc(t, i) * x);
+                p[i * S] = x;
+            }
+        }
+        __syncthreads();
+        // publish this step's edge rows into the other parity (read by the neighbours in step
+        // j+1, after its first cluster barrier; the parity read in step j is not touched)
+        if (DR) publish_edges(par ^ 1);
+    }
+    cl.sync();  // no CTA leaves while a neighbour may still read its shared memory
+    // ---- F^s(U) (or Delta_n = F^s(U) - G(U)) ----
+    for (int e = tid; e < SW_R * N / 2; e += SW_T) {
+        const int r = e / (N / 2), x2 = (e % (N / 2)) * 2;
+        const double *d = tile + r * S + cpad(x2);
+        const long long g = base + (long long)r * N + x2;
+        double2 o = make_double2(d[0], d[1]);
+        if (EPI == EPI_DELTA) {
+            const double2 gcv = __ldg(reinterpret_cast<const double2 *>(a.gc + g));
+            o.x -= gcv.x;
+            o.y -= gcv.y;
+        }
+        *reinterpret_cast<double2 *>(a.out + g) = o;
+    }
+}
+
+}  // namespace prs

@@ -597,3 +597,34 @@ def test_space_parallel_g_rejects_unsupported_shapes():
     ctx.set_coarse_mode(1, 4)
     ctx.set_coarse_mode(0)
     ctx.close()
+
+
+SWEEP2_CASES = [
+    synth.CONFIGS["c0"],
+    Problem(dim=2, n=64, c=1.0, N=5, s=4, G=DR, F=DR, init="modes", seed=7),
+    Problem(dim=2, n=64, c=1.0, source=1, N=3, s=5, G=FIE, F=FIE),
+    Problem(dim=2, n=128, c=2.0, N=4, s=3, G=FIE, F=DR, init="modes", seed=8),
+    Problem(dim=2, n=128, c=1.0, source=1, N=3, s=2, G=DR, F=FIE),
+    Problem(dim=2, n=256, c=1.0, N=3, s=4, G=FIE, F=DR, init="modes", seed=9),
+    Problem(dim=2, n=256, c=1.0, source=1, N=2, s=3, G=FIE, F=FIE),
+]
+
+
+@pytest.mark.parametrize("p", SWEEP2_CASES, ids=lambda p: p.label())
+def test_on_chip_sweep_matches_oracle(p):
+    """sweep2: the whole fine sweep of a small 2-D slice in one cluster's shared memory
+    (x rows CTA-local, y columns and DR halo rows through DSMEM): every parareal iterate
+    against the oracle."""
+    _parareal_vs_oracle(p)
+
+
+def test_on_chip_sweep_equals_per_step_kernels(monkeypatch):
+    """PRS_SWEEP2=0 runs the same sweep through the per-step kernels: same results to rounding."""
+    p = Problem(dim=2, n=256, c=1.0, N=4, s=6, G=DR, F=DR, init="modes", seed=3)
+    u0 = synth.initial_state(p)
+    a, _ = gpu_parareal(p, u0, 2)
+    monkeypatch.setenv("PRS_SWEEP2", "0")
+    b, _ = gpu_parareal(p, u0, 2)
+    scale = max(float(np.max(np.abs(t))) for t in b)
+    for k in range(3):
+        assert float(np.max(np.abs(a[k] - b[k]))) / scale <= TOL
