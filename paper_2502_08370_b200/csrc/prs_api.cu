@@ -4,6 +4,7 @@
 // context stream; L3 parareal driver = batched fine sweep over all local slices, sequential
 // coarse chain with the fused correction epilogue, stop test, NCCL hand-off of slice end
 // states between ranks (rank order = time order).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
@@ -131,6 +132,11 @@ struct prs_ctx {
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
     bool x3_contig = false;    // PRS_X3CONTIG=1: xpass3 takes one contiguous range per CTA
     bool no_sweep2 = false;    // PRS_SWEEP2=0: small 2-D slices step through the per-step kernels
+    bool x3_tma = false;       // PRS_X3TMA=1: xpass3 fills its ring by TMA tensor copies (one per
+                               // group, 128-byte swizzle) instead of 16-byte cp.async; measured
+                               // ~3% slower on c3 (the pass is bound by its row latency chain)
+    // TMA tensor maps (rows of 16 doubles, 128-byte swizzle) by (address, rows)
+    std::vector<std::pair<std::pair<const void *, long long>, CUtensorMap>> tmaps;
     bool no_tiled = true;      // PRS_TILED=1: 2-D long lines take lp9 x tiles + lp8 (opt-in:
                                // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
     double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
@@ -296,6 +302,47 @@ struct EpiArgs {
     double *traj = nullptr;
 };
 
+// ---- TMA tensor maps: a buffer of `rows` x 16 doubles (128-byte rows), box 16 x 256
+// (one 4096-double group), 128-byte swizzle; encoded through the driver entry point (no
+// link-time libcuda dependency) and cached per (address, rows)
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int get_tmap(prs_ctx *ctx, const void *ptr, long long rows, CUtensorMap *out) {
+    for (auto &e : ctx->tmaps)
+        if (e.first.first == ptr && e.first.second == rows) {
+            *out = e.second;
+            return PRS_OK;
+        }
+    static PFN_encodeTiled encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) {
+            ctx->err = "cuTensorMapEncodeTiled unavailable";
+            return PRS_ECUDA;
+        }
+        encode = reinterpret_cast<PFN_encodeTiled>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)LCH, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(LCH * sizeof(double))};
+    const cuuint32_t box[2] = {(cuuint32_t)LCH, (cuuint32_t)X3T};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptr), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        ctx->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+        return PRS_ECUDA;
+    }
+    if (ctx->tmaps.size() > 64) ctx->tmaps.clear();
+    ctx->tmaps.push_back({{ptr, rows}, m});
+    *out = m;
+    return PRS_OK;
+}
+
 // persistent pipelined x-pass (xpass3.cuh) when the shape allows it
 static bool xpass3_ok(const prs_ctx *ctx, long long B) {
     const int n = ctx->p.n;
@@ -344,9 +391,16 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     const int dr = (scheme == PRS_DR) ? 1 : 0;
     const int coef = ctx->p.coef_kind;
     const int src = ctx->p.source_kind;
-    const size_t shm = xpass3_smem_bytes(coef);
+    const size_t shm = xpass3_smem_bytes(coef, ctx->x3_tma ? 1 : 0);
     void (*kern)(X3Args) = nullptr;
-#define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass3_kernel<C, D, S_>;
+    const int tma = ctx->x3_tma ? 1 : 0;
+    if (tma) {
+        TRY(get_tmap(ctx, in, B * ctx->vol / LCH, &a.tm_in));
+        if (coef) TRY(get_tmap(ctx, f.invdx, (long long)n * n / LCH, &a.tm_piv));
+    }
+#define XK(C, D, S_)                                                                 \
+    if (coef == C && dr == D && src == S_)                                           \
+        kern = tma ? xpass3_kernel<C, D, S_, 1> : xpass3_kernel<C, D, S_, 0>;
     XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
 #undef XK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -1077,6 +1131,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *xbv = getenv("PRS_X3TMA");
+        ctx->x3_tma = xbv && xbv[0] == '1';
         const char *swv = getenv("PRS_SWEEP2");
         ctx->no_sweep2 = swv && swv[0] == '0';
         const char *x3c = getenv("PRS_X3CONTIG");
@@ -1447,10 +1503,14 @@ static int gp_phase1(prs_ctx *ctx, int b, const double *in, double *v, int slice
     x.s2f = ctx->s2f;
     const int coef = ctx->p.coef_kind, src = ctx->p.source_kind;
     void (*kx)(X3Args) = nullptr;
-#define XK(C, S_) if (coef == C && src == S_) kx = xpass3_kernel<C, 0, S_>;
+    if (ctx->x3_tma) {
+        TRY(get_tmap(ctx, in, x.vol / LCH, &x.tm_in));
+        if (coef) TRY(get_tmap(ctx, f.invdx, (long long)n * n / LCH, &x.tm_piv));
+    }
+#define XK(C, S_) if (coef == C && src == S_) kx = ctx->x3_tma ? xpass3_kernel<C, 0, S_, 1> : xpass3_kernel<C, 0, S_, 0>;
     XK(0, 0) XK(0, 1) XK(1, 0) XK(1, 1)
 #undef XK
-    const size_t shm = xpass3_smem_bytes(coef);
+    const size_t shm = xpass3_smem_bytes(coef, ctx->x3_tma ? 1 : 0);
     CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     kx<<<(unsigned)std::min<long long>(ctx->num_sms, x.ngroups), X3T, shm, ctx->stream>>>(x);
     TRY(last_launch(ctx));

@@ -14,6 +14,8 @@
 // DR's neighbour rows come from the same ring (row j-1 / j+1 of the previous / next group),
 // so every state row is read from HBM once per pass.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace prs {
@@ -23,6 +25,8 @@ constexpr int X3C = 18;         // shared stride of a chunk (16 + 2 pad, 16-byte
 constexpr int X3G = X3T * X3C;  // doubles per group buffer
 
 struct X3Args {
+    CUtensorMap tm_in;    // TMA: the input batch as rows of 16 doubles (128-byte swizzle), box 16 x 256
+    CUtensorMap tm_piv;   // TMA: the x pivots (variable kappa) likewise
     const double *in;
     double *out;
     long long vol;        // points per state
@@ -47,7 +51,8 @@ struct X3Args {
     const double *invd, *s2n, *s2f;
 };
 
-inline size_t xpass3_smem_bytes(int coef) {
+inline size_t xpass3_smem_bytes(int coef, int tma = 0) {
+    if (tma) return sizeof(double) * ((size_t)(4 + (coef ? 2 : 1)) * X3T * LCH) + 1024 + sizeof(double2) * 16;
     return sizeof(double) * ((size_t)(4 + (coef ? 2 : 1)) * X3G) + sizeof(double2) * 16;
 }
 
@@ -61,13 +66,32 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int COEF, int DR, int SRC>
-__global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
-    extern __shared__ __align__(16) double smem[];
-    double *ubuf = smem;                          // 4 x X3G ring of state groups
-    double *ibuf = smem + 4 * X3G;                // COEF: 2 x X3G pivot groups; else 1 x X3G out staging
-    double2 *scr = reinterpret_cast<double2 *>(smem + (4 + (COEF ? 2 : 1)) * X3G);
-
+// TMA = 1: every group (4096 doubles = 256 rows of 128 bytes) arrives as ONE 2-D tensor copy
+// issued by one thread, completing on the slot's mbarrier; the tensor map's 128-byte swizzle
+// puts 16-byte unit u of thread k's chunk (row k) at unit u ^ (k & 7), so the per-thread chunk
+// reads stay bank-conflict free without padding.  TMA = 0: 8 16-byte cp.async per thread per
+// group into the padded (stride-18) chunk layout.
+template <int COEF, int DR, int SRC, int TMA>
+__global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ X3Args a) {
+    extern __shared__ __align__(16) double smem_raw[];
+    // TMA: slots 1024-byte aligned (swizzle atom), unpadded
+    double *smem = TMA ? reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023)
+                       : smem_raw;
+    constexpr int SLOT = TMA ? X3T * LCH : X3G;  // doubles per ring slot
+    __shared__ __align__(8) unsigned long long mbu[4], mbp[2];  // TMA: per ring slot
+    if (TMA && threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(mbu + i, 1);
+        for (int i = 0; i < 2; ++i) mbar_init(mbp + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    unsigned npu = 0, npp = 0;       // TMA: parity the next fill of each slot will complete (bits)
+    unsigned filledu = 0, filledp = 0;
+    // offset (doubles) of 16-byte unit u of chunk (row) r within a slot
+    auto uoff = [&](int r, int u) { return TMA ? r * LCH + ((u ^ (r & 7)) << 1) : r * X3C + 2 * u; };
+    double *ubuf = smem;                          // 4 slots: ring of state groups
+    double *ibuf = smem + 4 * SLOT;               // COEF: 2 pivot slots; else 1 out staging slot
+    double2 *scr = reinterpret_cast<double2 *>(smem + (4 + (COEF ? 2 : 1)) * SLOT);
     const int k = threadIdx.x;
     const int P = a.P, n = a.n;
     const int lpg = X3T / P;  // lines per group
@@ -113,8 +137,30 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
     }
     __syncthreads();  // the previous range's buffers are free
 
-    // issue the 16-byte copies of group g of a row-major source into a chunk-layout buffer
-    auto issue_group = [&](const double *src, long long g, double *dst) {
+    // issue the copies of group g into a slot: TMA (one thread, one tensor copy; `trow` = the
+    // tensor row of the group's first 128-byte row) or cp.async (all threads)
+    auto issue_group = [&](const double *src, long long g, double *dst, const CUtensorMap *tm, long long trow) {
+        if (TMA) {
+            const int slot = (int)((dst - ubuf) / SLOT);  // state ring 0..3, pivot ring 4..5
+            unsigned long long *mb = (slot < 4) ? mbu + slot : mbp + (slot - 4);
+            if (slot < 4) {
+                npu ^= 1u << slot;
+                filledu |= 1u << slot;
+            } else {
+                npp ^= 1u << (slot - 4);
+                filledp |= 1u << (slot - 4);
+            }
+            if (k == 0) {
+                mbar_arrive_expect(mb, (unsigned)(group_elems * sizeof(double)));
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                    "l"(reinterpret_cast<unsigned long long>(tm)), "r"(0), "r"((int)trow),
+                    "r"((unsigned)__cvta_generic_to_shared(mb))
+                    : "memory");
+            }
+            return;
+        }
         const double *s = src + g * group_elems;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -123,25 +169,35 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
             cp_async16(dst + c * X3C + 2 * u, s + 2 * p);
         }
     };
+    // TMA: wait until the most recent fill of a slot has landed (parity of that fill)
+    auto wait_u = [&](long long g) {
+        const int sl = (int)(g & 3);
+        if (TMA && ((filledu >> sl) & 1)) mbar_wait(mbu + sl, ((npu >> sl) & 1) ^ 1);
+    };
+    auto wait_p = [&](long long g) {
+        const int sl = COEF ? (int)(g & 1) : 0;
+        if (TMA && COEF && ((filledp >> sl) & 1)) mbar_wait(mbp + sl, ((npp >> sl) & 1) ^ 1);
+    };
     // state groups are contiguous in memory across the whole batch: group g = elements
     // [g*4096, (g+1)*4096) of the batch buffer; a group never splits a line (n | 4096).
     const double *pin = a.in;
-    auto ub = [&](long long g) { return ubuf + (int)(g & 3) * X3G; };
-    auto ib = [&](long long g) { return ibuf + (COEF ? (int)(g & 1) : 0) * X3G; };
+    auto ub = [&](long long g) { return ubuf + (int)(g & 3) * SLOT; };
+    auto ib = [&](long long g) { return ibuf + (COEF ? (int)(g & 1) : 0) * SLOT; };
+    auto issue_state = [&](long long g) { issue_group(pin, g, ub(g), &a.tm_in, g * (group_elems / LCH)); };
     // pivot rows repeat every state: the group of pivots for global group g starts at
     // row (g * lpg) mod lines_per_state
     auto issue_piv = [&](long long g) {
         const long long row0 = ((g * lpg) & (a.lines_per_state - 1)) + a.row0;
-        issue_group(a.invd + row0 * n - 0, 0, ib(g));
+        issue_group(a.invd + row0 * n - 0, 0, ib(g), &a.tm_piv, row0 * n / LCH);
     };
 
     // prologue: U(g0-1) (DR halo), U(g0), U(g0+1), pivots(g0)
     if (g0 < g1) {
-        if (DR && g0 > 0) issue_group(pin, g0 - 1, ub(g0 - 1));
-        issue_group(pin, g0, ub(g0));
+        if (DR && g0 > 0) issue_state(g0 - 1);
+        issue_state(g0);
         if (COEF) issue_piv(g0);
         cp_async_commit();
-        if (g0 + 1 < G) issue_group(pin, g0 + 1, ub(g0 + 1));
+        if (g0 + 1 < G) issue_state(g0 + 1);
         cp_async_commit();
     }
 
@@ -177,10 +233,17 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         const LineScalars cur = nxt;
         nxt = line_scalars(g + 1);
         // prefetch two ahead (state) / one ahead (pivots)
-        if (g + 2 < G && g + 2 < g1 + (DR ? 1 : 0)) issue_group(pin, g + 2, ub(g + 2));
+        if (g + 2 < G && g + 2 < g1 + (DR ? 1 : 0)) issue_state(g + 2);
         if (COEF && g + 1 < g1) issue_piv(g + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
+        if (TMA) {
+            if (DR && g > 0) wait_u(g - 1);
+            wait_u(g);
+            if (DR && g + 1 < G) wait_u(g + 1);
+            if (COEF) wait_p(g);
+        } else {
+            cp_async_commit();
+            cp_async_wait<1>();
+        }
         __syncthreads();
 
         // line of this thread: global line index, state, row
@@ -189,23 +252,24 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         const double *U = ub(g);
         double v[LCH], w[LCH];
         {
-            const double *src = U + k * X3C;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const double2 x = *reinterpret_cast<const double2 *>(src + 2 * u);
+                const double2 x = *reinterpret_cast<const double2 *>(U + uoff(k, u));
                 v[2 * u] = x.x;
                 v[2 * u + 1] = x.y;
             }
         }
         if (DR) {  // w = tau A_y U with rows j-1, j+1 from the ring (2-D)
             const bool hm = j > 0, hp = j < n - 1;
-            const double *um = (l > 0) ? U + (k - P) * X3C : ub(g - 1) + (k - P + X3T) * X3C;
-            const double *up = (l < lpg - 1) ? U + (k + P) * X3C : ub(g + 1) + (k + P - X3T) * X3C;
+            // rows (chunks) of the neighbour lines in this group's slot or the previous / next one
+            const double *ums = (l > 0) ? U : ub(g - 1);
+            const double *ups = (l < lpg - 1) ? U : ub(g + 1);
+            const int rm = (l > 0) ? k - P : k - P + X3T, rp = (l < lpg - 1) ? k + P : k + P - X3T;
             const double kfm = 0.5 * cur.kfm, kfp = 0.5 * cur.kfp;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const double2 xm = hm ? *reinterpret_cast<const double2 *>(um + 2 * u) : make_double2(0.0, 0.0);
-                const double2 xp = hp ? *reinterpret_cast<const double2 *>(up + 2 * u) : make_double2(0.0, 0.0);
+                const double2 xm = hm ? *reinterpret_cast<const double2 *>(ums + uoff(rm, u)) : make_double2(0.0, 0.0);
+                const double2 xp = hp ? *reinterpret_cast<const double2 *>(ups + uoff(rp, u)) : make_double2(0.0, 0.0);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int i = 2 * u + h;
@@ -227,14 +291,14 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         // (registers) times the per-point inverse pivots of this group
         double idr[LCH], idm1 = 0.0, hsx = 0.0;
         if (COEF) {
-            const double *I = ib(g) + k * X3C;
+            const double *I = ib(g);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const double2 x = *reinterpret_cast<const double2 *>(I + 2 * u);
+                const double2 x = *reinterpret_cast<const double2 *>(I + uoff(k, u));
                 idr[2 * u] = x.x;
                 idr[2 * u + 1] = x.y;
             }
-            idm1 = (t > 0) ? I[-X3C + LCH - 1] : 0.0;
+            idm1 = (t > 0) ? I[uoff(k - 1, 7) + 1] : 0.0;  // last element of the previous chunk
             hsx = 0.5 * cur.hsx;
         }
         auto af = [&](int i) { return -tauh * fma(hsx, sf[i], 1.0); };
@@ -292,9 +356,10 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
         }
         __syncthreads();  // every read of ib(g) / scr done
         {
-            double *dst = ib(g) + k * X3C;
+            double *dst = ib(g);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) *reinterpret_cast<double2 *>(dst + 2 * u) = make_double2(v[2 * u], v[2 * u + 1]);
+            for (int u = 0; u < 8; ++u)
+                *reinterpret_cast<double2 *>(dst + uoff(k, u)) = make_double2(v[2 * u], v[2 * u + 1]);
         }
         __syncthreads();
         {
@@ -304,13 +369,24 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(X3Args a) {
             for (int q = 0; q < 8; ++q) {
                 const int p = k + q * X3T;
                 const int c = p >> 3, u = p & 7;
-                const double2 xx = *reinterpret_cast<const double2 *>(src + c * X3C + 2 * u);
+                const double2 xx = *reinterpret_cast<const double2 *>(src + uoff(c, u));
                 *reinterpret_cast<double2 *>(o + 2 * p) = xx;
             }
         }
+        // the staging slot gets the next pivot group by TMA: order these generic accesses
+        // before the async proxy's writes
+        if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();  // staging buffer free before the next prefetch lands in it
     }
-    cp_async_wait<0>();
+    if (TMA) {  // every fill issued in this range has landed before the slots are reused
+        for (int sl = 0; sl < 4; ++sl)
+            if ((filledu >> sl) & 1) mbar_wait(mbu + sl, ((npu >> sl) & 1) ^ 1);
+        if (COEF)
+            for (int sl = 0; sl < 2; ++sl)
+                if ((filledp >> sl) & 1) mbar_wait(mbp + sl, ((npp >> sl) & 1) ^ 1);
+    } else {
+        cp_async_wait<0>();
+    }
     }  // tasks
 }
 

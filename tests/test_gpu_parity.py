@@ -628,3 +628,26 @@ def test_on_chip_sweep_equals_per_step_kernels(monkeypatch):
     scale = max(float(np.max(np.abs(t))) for t in b)
     for k in range(3):
         assert float(np.max(np.abs(a[k] - b[k]))) / scale <= TOL
+
+
+@pytest.mark.parametrize("p", [Problem(dim=2, n=4096, c=1.0, coef=1, N=2, s=2, G=FIE, F=DR, init="modes", seed=3),
+                               Problem(dim=2, n=256, c=1.0, coef=1, N=4, s=3, G=DR, F=FIE, source=1)],
+                         ids=lambda p: p.label())
+def test_xpass3_tma_ring_matches_cp_async(p, monkeypatch):
+    """PRS_X3TMA=1: xpass3's ring filled by one TMA tensor copy per group (128-byte swizzle,
+    mbarrier completion) gives the same fine step as the cp.async ring, to rounding."""
+    prs = prs_mod()
+    B = 2
+    base = synth.initial_state(p)
+    us = np.stack([base * (1.0 + 0.5 * b) + 1e-3 * rand_field(p, 90 + b) for b in range(B)])
+    outs = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PRS_X3TMA", mode)
+        ctx = prs.Context(p)
+        du = dev(us)
+        out = torch.empty_like(du)
+        ctx.step_batch(1, 0, 1, du, out, B)
+        outs.append(host(out))
+        ctx.close()
+    scale = max(float(np.max(np.abs(outs[1]))), float(np.max(np.abs(us))))
+    assert float(np.max(np.abs(outs[0] - outs[1]))) / scale <= 1e-13
