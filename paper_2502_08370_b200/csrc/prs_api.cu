@@ -1274,6 +1274,9 @@ int prs_set_initial(prs_ctx *ctx, const double *u0, int u0_on_device) {
     return PRS_OK;
 }
 
+static bool sweep2_ok(const prs_ctx *ctx);
+static int launch_chain2(prs_ctx *ctx, int i0, int epi);
+
 static TimeArgs coarse_time(prs_ctx *ctx, int slice) {
     TimeArgs ta;
     ta.slice0 = slice;
@@ -1289,7 +1292,8 @@ int prs_coarse_sweep(prs_ctx *ctx) {
     TRY(ensure_factors(ctx, 0, ctx->dT));
     if (ctx->nranks > 1 && ctx->rank > 0)
         NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-    for (int i = 0; i < ctx->count; ++i) {
+    if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, 0, EPI_INIT));
+    for (int i = sweep2_ok(ctx) ? ctx->count : 0; i < ctx->count; ++i) {
         EpiArgs ep;
         ep.kind = EPI_INIT;
         ep.gcache = state(ctx, ctx->gcache, i);
@@ -1367,6 +1371,63 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
     // 32 B per update for a 2-D step; on chip here, so the rate is an effective one
     if (ctx->prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * ctx->p.s * 32.0));
     return PRS_OK;
+}
+
+// the coarse chain of local slices i0 .. count-1 on chip (sweep2 with CHAIN = 1): one cluster
+static int launch_chain2(prs_ctx *ctx, int i0, int epi) {
+    const int n = ctx->p.n, cnt = ctx->count - i0;
+    if (cnt <= 0) return PRS_OK;
+    const TauFactors &f = ctx->fac[0];
+    SWArgs a{};
+    a.in = state(ctx, ctx->traj, i0);
+    a.traj = state(ctx, ctx->traj, i0);
+    a.gcache = state(ctx, ctx->gcache, i0);
+    a.delta = (epi == EPI_CORRECT) ? state(ctx, ctx->delta, i0) : nullptr;
+    a.red = ctx->red;
+    a.vol = ctx->ss;
+    a.s = cnt;
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.creact = ctx->creact;
+    a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
+    a.sinpi = ctx->sinpi;
+    a.slice0 = ctx->first + i0;
+    a.dt = ctx->dT;
+    a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
+    const int dr = (ctx->p.G == PRS_DR) ? 1 : 0, src = ctx->p.source_kind;
+    void (*k)(SWArgs) = nullptr;
+    size_t shm = 0;
+#define SK(N_, D, S_, E)                                                   \
+    if (n == N_ && dr == D && src == S_ && epi == E) {                     \
+        k = sweep2_kernel<N_, D, S_, E, 1>;                                \
+        shm = sizeof(double) * sweep2_smem_doubles<N_>();                   \
+    }
+#define SKN(N_) SK(N_, 0, 0, EPI_CORRECT) SK(N_, 0, 1, EPI_CORRECT) SK(N_, 1, 0, EPI_CORRECT) \
+                SK(N_, 1, 1, EPI_CORRECT) SK(N_, 0, 0, EPI_INIT) SK(N_, 0, 1, EPI_INIT)       \
+                SK(N_, 1, 0, EPI_INIT) SK(N_, 1, 1, EPI_INIT)
+    SKN(32) SKN(64) SKN(128) SKN(256)
+#undef SKN
+#undef SK
+    if (!k) {
+        ctx->err = "chain2: unsupported shape";
+        return PRS_EUNSUPPORTED;
+    }
+    const int CL = n / SW_R;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)CL);
+    cfg.blockDim = dim3(SW_T);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, a));
+    return last_launch(ctx);
 }
 
 static int enqueue_fine_sweep(prs_ctx *ctx) {
@@ -1642,6 +1703,7 @@ static int gp_correct(prs_ctx *ctx) {
 // epilogue for every local slice, in time order
 static int enqueue_correct_chain(prs_ctx *ctx) {
     CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
+    if (sweep2_ok(ctx)) return launch_chain2(ctx, local_start(ctx), EPI_CORRECT);
     for (int i = local_start(ctx); i < ctx->count; ++i) {
         EpiArgs ep;
         ep.kind = EPI_CORRECT;
@@ -1665,7 +1727,8 @@ int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
         CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
         if (ctx->rank > 0)
             NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-        for (int i = local_start(ctx); i < ctx->count; ++i) {
+        if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, local_start(ctx), EPI_CORRECT));
+        for (int i = sweep2_ok(ctx) ? ctx->count : local_start(ctx); i < ctx->count; ++i) {
             EpiArgs ep;
             ep.kind = EPI_CORRECT;
             ep.gcache = state(ctx, ctx->gcache, i);

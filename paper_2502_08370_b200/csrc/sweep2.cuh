@@ -13,6 +13,10 @@
 //    the CTA totals per column are exchanged through distributed shared memory (every CTA
 //    composes the totals of the CTAs before and after it), then the exact recurrences.
 // Pivot tables (kappa = 1: the same for x and y) sit chunk-padded in shared memory.
+// CHAIN = 1 reuses the step for the coarse chain of the parareal correction:
+// one cluster advances U_i -> G(U_i) slice after slice with the state on chip, applying the
+// fused correction (G cache, U_{i+1} = G(U_i) + Delta_i, update max, non-finite flag) after
+// every step; the initial guess (EPI_INIT) likewise.
 #pragma once
 #include "common.cuh"
 #include "lpass.cuh"
@@ -24,9 +28,15 @@ constexpr int SW_R = 32;   // rows per CTA
 constexpr int SW_T = 256;  // threads per CTA
 
 struct SWArgs {
-    const double *in;     // U^k_n of the batch (slice stride vol)
+    const double *in;     // fine sweep: U^k_n of the batch (slice stride vol); chain: U_{i0}
     double *out;          // Delta_n (EPI_DELTA) or F^s(U) (EPI_STORE)
     const double *gc;     // G cache (EPI_DELTA)
+    // coarse chain (CHAIN = 1): one cluster runs the s G steps of slices i0 .. i0+s-1 in turn,
+    // U_{i+1} <- G(U_i) (+ Delta_i, EPI_CORRECT), the G cache of slice i <- G(U_i)
+    double *traj;         // U_i of local slice i at traj + i vol
+    double *gcache;
+    const double *delta;
+    unsigned long long *red;  // [0] max |update| bits, [1] non-finite flag (EPI_CORRECT)
     long long vol;
     int s;                // fine steps
     double tau, h2inv, creact, src_amp;
@@ -46,7 +56,7 @@ constexpr size_t sweep2_smem_doubles() {
            5 * N + 2 * 2 * (N + N / LCH);
 }
 
-template <int N, int DR, int SRC, int EPI>
+template <int N, int DR, int SRC, int EPI, int CHAIN = 0>
 __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
     constexpr int CL = N / SW_R;      // CTAs per slice
     constexpr int S = N + N / LCH;    // padded row stride
@@ -97,6 +107,8 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
     }
     const double tauh = a.tau * a.h2inv, taucr = a.tau * a.creact;
     constexpr int NXT = (XT + SW_T - 1) / SW_T, NYT = (YT + SW_T - 1) / SW_T;
+    double cdmax = 0.0;         // CHAIN, EPI_CORRECT: max |U^{k+1} - U^k| of this thread's points
+    unsigned long long cbad = 0;
 
     for (int j = 0; j < a.s; ++j) {
         cl.sync();  // previous step complete in every CTA (edge rows published, remote totals consumed)
@@ -133,7 +145,8 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
 #pragma unroll
             for (int i = 0; i < LCH; ++i) v[i] = DR ? p[i] + w[k][i] : p[i];
             if (SRC) {
-                const double t = (double)((a.slice0 + b) * a.s + j + 1) * a.dt;
+                const double t = CHAIN ? (double)(a.slice0 + j + 1) * a.dt
+                                       : (double)((a.slice0 + b) * a.s + j + 1) * a.dt;
                 const double f = a.tau * a.src_amp * exp(-t) * __ldg(a.sinpi + r0 + r);
 #pragma unroll
                 for (int i = 0; i < LCH; ++i) v[i] = fma(f, __ldg(a.sinpi + c * LCH + i), v[i]);
@@ -272,11 +285,49 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
             }
         }
         __syncthreads();
+        if (CHAIN) {
+            // the correction of slice j: g = G(U_j) in the tile; the G cache,
+            // U_{j+1} = g + Delta_j (EPI_CORRECT) or g (EPI_INIT); the tile carries U_{j+1} on
+            for (int e = tid; e < SW_R * N / 2; e += SW_T) {
+                const int r = e / (N / 2), x2 = (e % (N / 2)) * 2;
+                double *d = tile + r * S + cpad(x2);
+                const long long off = (long long)r0 * N + (long long)r * N + x2;
+                const double2 gv = make_double2(d[0], d[1]);
+                *reinterpret_cast<double2 *>(a.gcache + (long long)j * a.vol + off) = gv;
+                double2 nv = gv;
+                if (EPI == EPI_CORRECT) {
+                    const double2 dv = *reinterpret_cast<const double2 *>(a.delta + (long long)j * a.vol + off);
+                    const double2 ov = *reinterpret_cast<const double2 *>(a.traj + (long long)(j + 1) * a.vol + off);
+                    nv.x += dv.x;
+                    nv.y += dv.y;
+                    cdmax = fmax(cdmax, fmax(fabs(nv.x - ov.x), fabs(nv.y - ov.y)));
+                    if (!isfinite(nv.x) || !isfinite(nv.y)) cbad = 1;
+                    d[0] = nv.x;
+                    d[1] = nv.y;
+                }
+                *reinterpret_cast<double2 *>(a.traj + (long long)(j + 1) * a.vol + off) = nv;
+            }
+            __syncthreads();
+        }
         // publish this step's edge rows into the other parity (read by the neighbours in step
         // j+1, after its first cluster barrier; the parity read in step j is not touched)
         if (DR) publish_edges(par ^ 1);
     }
     cl.sync();  // no CTA leaves while a neighbour may still read its shared memory
+    if (CHAIN) {
+        if (EPI == EPI_CORRECT) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                cdmax = fmax(cdmax, __shfl_xor_sync(0xffffffffu, cdmax, off));
+                cbad |= __shfl_xor_sync(0xffffffffu, cbad, off);
+            }
+            if (lane == 0) {
+                atomicMax(a.red, (unsigned long long)__double_as_longlong(cdmax));
+                if (cbad) atomicOr(a.red + 1, 1ull);
+            }
+        }
+        return;
+    }
     // ---- F^s(U) (or Delta_n = F^s(U) - G(U)) ----
     for (int e = tid; e < SW_R * N / 2; e += SW_T) {
         const int r = e / (N / 2), x2 = (e % (N / 2)) * 2;
