@@ -1321,7 +1321,8 @@ static bool sweep2_ok(const prs_ctx *ctx) {
            (n == 32 || n == 64 || n == 128 || n == 256);
 }
 
-static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const double *gc, long long B, long long slice0) {
+static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const double *gc, long long B, long long slice0,
+                         int steps) {
     const int n = ctx->p.n;
     const TauFactors &f = ctx->fac[1];
     SWArgs a{};
@@ -1329,7 +1330,7 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
     a.out = out;
     a.gc = gc;
     a.vol = ctx->ss;
-    a.s = ctx->p.s;
+    a.s = steps;
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.creact = ctx->creact;
@@ -1437,7 +1438,7 @@ static int enqueue_fine_sweep(prs_ctx *ctx) {
     if (B <= 0) return PRS_OK;
     if (sweep2_ok(ctx))
         return launch_sweep2(ctx, state(ctx, ctx->traj, i0), state(ctx, (s & 1) ? ctx->fa : ctx->fb, i0),
-                             state(ctx, ctx->gcache, i0), B, ctx->first + i0);
+                             state(ctx, ctx->gcache, i0), B, ctx->first + i0, s);
     const double *src = state(ctx, ctx->traj, i0);
     double *bufs[2] = {state(ctx, ctx->fa, i0), state(ctx, ctx->fb, i0)};
     for (int j = 0; j < s; ++j) {
@@ -1832,6 +1833,12 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
                        ctx->stream));
     int cur = 0;
     const int s = ctx->p.s;
+    if (sweep2_ok(ctx) && nslices > 0) {
+        // small 2-D states: all nslices * s steps in one on-chip sweep (source times (j+1) dt)
+        TRY(launch_sweep2(ctx, buf[0], buf[1], nullptr, 1, 0, nslices * s));
+        cur = 1;
+        nslices = 0;
+    }
     for (int n = 0; n < nslices; ++n) {
         for (int j = 0; j < s; ++j) {
             TimeArgs ta;

@@ -429,6 +429,7 @@ def test_c1_full_size_first_iterations():
 
 
 @pytest.mark.parametrize("p", [synth.CONFIGS["c0"],
+                               Problem(dim=2, n=128, c=1.0, N=4, s=3, G=FIE, F=DR, init="modes", seed=5),
                                Problem(dim=2, n=48, c=1.0, coef=1, N=6, s=5, G=FIE, F=DR, init="modes", seed=7),
                                Problem(dim=3, n=20, c=1.0, source=1, N=4, s=3),
                                Problem(dim=2, n=64, c=1.0, split=1, dd_strips=8, dd_overlap=4, source=1, N=4,
