@@ -30,6 +30,7 @@
 #include "xy3.cuh"
 #include "gpar.cuh"
 #include "sweep2.cuh"
+#include "xpass7.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -132,6 +133,7 @@ struct prs_ctx {
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
     bool x3_contig = false;    // PRS_X3CONTIG=1: xpass3 takes one contiguous range per CTA
     bool no_sweep2 = false;    // PRS_SWEEP2=0: small 2-D slices step through the per-step kernels
+    bool no_x7 = false;        // PRS_X7=0: 4096-point rows take xpass3 instead of the 2-CTA xpass7
     bool x3_tma = false;       // PRS_X3TMA=1: xpass3 fills its ring by TMA tensor copies (one per
                                // group, 128-byte swizzle) instead of 16-byte cp.async; measured
                                // ~3% slower on c3 (the pass is bound by its row latency chain)
@@ -412,8 +414,63 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     return PRS_OK;
 }
 
+// 4096-point rows (c3): each row over a 2-CTA cluster (xpass7.cuh)
+static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out, long long B,
+                         const TimeArgs &ta, bool prof) {
+    X7Args a{};
+    a.in = in;
+    a.out = out;
+    a.vol = ctx->vol;
+    a.nrows = B * (long long)X7N;
+    a.nstates = (int)B;
+    const long long ncl = ctx->num_sms;  // one cluster per SM pair slot: 2 CTAs per SM
+    a.nranges = 0;
+    if (!ctx->x3_contig && B > 1) {
+        long long g = ncl, bb = B;
+        while (bb) { const long long t = g % bb; g = bb; bb = t; }
+        const long long R = ncl / g;
+        if (X7N / R >= 64) a.nranges = (int)R;
+    }
+    a.tau = f.tau;
+    a.h2inv = ctx->h2inv;
+    a.creact = ctx->creact;
+    a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
+    a.sinpi = ctx->sinpi;
+    a.ta = ta;
+    a.tab = CoefTab{f.tab, f.tab ? f.tab + X7N : nullptr, f.tab ? f.tab + 2 * X7N : nullptr};
+    a.invd = f.invdx;
+    a.s2n = ctx->s2n;
+    a.s2f = ctx->s2f;
+    const int dr = (scheme == PRS_DR) ? 1 : 0, coef = ctx->p.coef_kind, src = ctx->p.source_kind;
+    void (*kern)(X7Args) = nullptr;
+#define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass7_kernel<C, D, S_>;
+    XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
+#undef XK
+    const size_t shm = xpass7_smem_bytes(coef);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * std::min<long long>(ncl, a.nrows)));
+    cfg.blockDim = dim3(X7T);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (prof) TRY(prof_begin(ctx));
+    CK(cudaLaunchKernelEx(&cfg, kern, a));
+    TRY(last_launch(ctx));
+    if (prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * (16.0 + (coef ? 8.0 : 0.0))));
+    return PRS_OK;
+}
+
 static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
                         long long B, const TimeArgs &ta, bool prof) {
+    if (!ctx->no_x7 && !ctx->force_v2 && ctx->p.dim == 2 && ctx->p.n == X7N && ctx->ss == ctx->vol)
+        return launch_xpass7(ctx, scheme, f, in, out, B, ta, prof);
     if (xpass3_ok(ctx, B)) return launch_xpass3(ctx, scheme, f, in, out, B, ta, prof);
     const int n = ctx->p.n, dim = ctx->p.dim;
     XArgs a{};
@@ -1131,6 +1188,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *x7v = getenv("PRS_X7");
+        ctx->no_x7 = x7v && x7v[0] == '0';
         const char *xbv = getenv("PRS_X3TMA");
         ctx->x3_tma = xbv && xbv[0] == '1';
         const char *swv = getenv("PRS_SWEEP2");
