@@ -129,6 +129,14 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
  *   n % (64 P) == 0 (PRS_EUNSUPPORTED otherwise).  Results equal owner-G up to rounding. */
 int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands);
 
+/* Host only (no GPU): the band exchange of space-parallel G for `rank` of nranks and N slices,
+ * phase 0 (scatter of Delta bands from the slice owners) or 1 (gather of U / G-cache bands back
+ * to them), as the point-to-point operations prs_parareal_correct issues (NCCL group).  Writes
+ * up to max_ops records of 6 ints {kind: 0 send, 1 recv, 2 local copy; what: 0 Delta_slice,
+ * 1 U_{slice+1}, 2 Gcache_slice; slice; band; peer rank; owner-side local state index} to ops
+ * (may be NULL) and returns the number of records, or -1 on bad arguments. */
+int prs_gpar_plan(int N, int nranks, int rank, int phase, int *ops, int max_ops);
+
 /* Counters.  prs_launches: kernels this context has launched so far.  With profiling on,
  * every fine-sweep kernel launch is bracketed by CUDA events on the context stream and
  * prs_kernel_stats(kind) returns, for kind PRS_K_XPASS (contiguous-axis line solve),

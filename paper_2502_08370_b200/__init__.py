@@ -20,7 +20,7 @@ PRS_FIE, PRS_DR = 0, 1
 PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
 EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
-           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
+           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_gpar_plan", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
            "prs_last_error", "prs_destroy"]
 
 
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
             "prs_step_batch": ([V, I, I, I, V, V, I], I),
             "prs_fine_solve": ([V, V, I, I, V, I], I),
             "prs_set_coarse_mode": ([V, I, I], I),
+            "prs_gpar_plan": ([I, I, I, I, PI, I], I),
             "prs_set_profiling": ([V, I], I),
             "prs_launches": ([V], ctypes.c_longlong),
             "prs_kernel_stats": ([V, I, PL, PD, PD], I),
@@ -93,6 +94,18 @@ def partition(N: int, nranks: int, rank: int):
     if rc != PRS_OK:
         raise PrsError(rc, "bad partition arguments")
     return first.value, count.value
+
+
+def gpar_plan(N: int, nranks: int, rank: int, phase: int):
+    """Space-parallel G band exchange of `rank` (host logic, no GPU): list of
+    (kind, what, slice, band, peer, local_index) records, see include/prs.h."""
+    L = lib()
+    cnt = L.prs_gpar_plan(N, nranks, rank, phase, None, 0)
+    if cnt < 0:
+        raise PrsError(PRS_EINVAL, "bad gpar_plan arguments")
+    buf = (ctypes.c_int * (6 * max(cnt, 1)))()
+    L.prs_gpar_plan(N, nranks, rank, phase, buf, cnt)
+    return [tuple(buf[6 * i: 6 * i + 6]) for i in range(cnt)]
 
 
 def nccl_unique_id() -> bytes:

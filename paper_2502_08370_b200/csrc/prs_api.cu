@@ -1667,6 +1667,59 @@ static int gp_phase2(prs_ctx *ctx, int b, double *v, double *traj_next, double *
     return PRS_OK;
 }
 
+// The band exchange of space-parallel G over P = nranks ranks as a list of point-to-point
+// operations (host logic, also exported as prs_gpar_plan for the multi-process tests): each op is
+// {kind (0 send, 1 recv, 2 local copy), what (0 Delta_slice, 1 U_{slice+1}, 2 Gcache_slice),
+//  slice, band, peer, local index of the owner-side state}; the ops between any two ranks come
+// in the same order on both sides (NCCL group / in-order matching).
+//   phase 0 (scatter): band p of Delta_sl from owner(sl) to rank p;
+//   phase 1 (gather) : band p of U_{sl+1} to owner(sl) (its end state) and, at a rank edge, to
+//                      owner(sl+1) (its incoming state, local index 0); band p of Gcache_sl to
+//                      owner(sl).
+static int gpar_plan(int N, int nranks, int me, int phase, std::vector<int> &ops) {
+    ops.clear();
+    const int P = nranks;
+    std::vector<int> own(N), first(P);
+    for (int q = 0; q < P; ++q) {
+        int f0 = 0, c0 = 0;
+        if (prs_partition(N, P, q, &f0, &c0) != PRS_OK) return PRS_EINVAL;
+        first[q] = f0;
+        for (int sl = f0; sl < f0 + c0; ++sl) own[sl] = q;
+    }
+    auto push = [&](int kind, int what, int sl, int band, int peer, int lidx) {
+        ops.insert(ops.end(), {kind, what, sl, band, peer, lidx});
+    };
+    if (phase == 0) {
+        for (int sl = 0; sl < N; ++sl) {
+            const int q = own[sl];
+            if (q == me) {
+                for (int p = 0; p < P; ++p) push(p == me ? 2 : 0, 0, sl, p, p, sl - first[q]);
+            } else {
+                push(1, 0, sl, me, q, -1);
+            }
+        }
+        return PRS_OK;
+    }
+    for (int sl = 0; sl < N; ++sl) {
+        const int q = own[sl];
+        const int qn = (sl + 1 < N) ? own[sl + 1] : -1;
+        for (int p = 0; p < P; ++p) {
+            const int dsts[2] = {q, (qn != q) ? qn : -1};
+            for (int dst : dsts) {
+                if (dst < 0) continue;
+                const int lidx = (dst == q) ? sl + 1 - first[q] : 0;
+                if (p == me && dst == me) push(2, 1, sl, p, me, lidx);
+                else if (p == me) push(0, 1, sl, p, dst, lidx);
+                else if (dst == me) push(1, 1, sl, p, p, lidx);
+            }
+            if (p == me && q == me) push(2, 2, sl, p, me, sl - first[q]);
+            else if (p == me) push(0, 2, sl, p, q, sl - first[q]);
+            else if (q == me) push(1, 2, sl, p, p, sl - first[q]);
+        }
+    }
+    return PRS_OK;
+}
+
 // the correction chain with space-parallel G.  One process: every slice, all P bands are
 // views into the full states.  P ranks: this rank's band of every state, Delta bands
 // scattered from the slice owners first, U / G-cache bands gathered back afterwards.
@@ -1688,29 +1741,20 @@ static int gp_correct(prs_ctx *ctx) {
     const int me = ctx->rank, N = ctx->p.N;
     // U_0's band (U^{k+1}_0 = U_0)
     CK(cudaMemcpyAsync(ctx->gb_u, ctx->u0 + (long long)me * bvol, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
-    auto owner = [&](int slice) {
-        for (int q = 0; q < ctx->nranks; ++q) {
-            int f0 = 0, c0 = 0;
-            prs_partition(N, ctx->nranks, q, &f0, &c0);
-            if (slice >= f0 && slice < f0 + c0) return q;
-        }
-        return -1;
-    };
     // scatter: band p of Delta_n from owner(n) to rank p
+    std::vector<int> ops;
+    TRY(gpar_plan(N, ctx->nranks, me, 0, ops));
     NK(g_nccl.GroupStart());
-    for (int sl = 0; sl < N; ++sl) {
-        const int q = owner(sl);
-        if (q == me) {
-            const double *d = state(ctx, ctx->delta, sl - ctx->first);
-            for (int p = 0; p < P; ++p) {
-                if (p == me)
-                    CK(cudaMemcpyAsync(ctx->gb_d + sl * bvol, d + p * bvol, bbytes, cudaMemcpyDeviceToDevice,
-                                       ctx->stream));
-                else
-                    NK(g_nccl.Send(d + p * bvol, (size_t)bvol, ncclDouble, p, ctx->comm, ctx->stream));
-            }
+    for (size_t o = 0; o < ops.size(); o += 6) {
+        const int kind = ops[o], sl = ops[o + 2], band = ops[o + 3], peer = ops[o + 4], lidx = ops[o + 5];
+        if (kind == 1) {
+            NK(g_nccl.Recv(ctx->gb_d + sl * bvol, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
         } else {
-            NK(g_nccl.Recv(ctx->gb_d + sl * bvol, (size_t)bvol, ncclDouble, q, ctx->comm, ctx->stream));
+            const double *d = state(ctx, ctx->delta, lidx) + band * bvol;
+            if (kind == 2)
+                CK(cudaMemcpyAsync(ctx->gb_d + sl * bvol, d, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+            else
+                NK(g_nccl.Send(d, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
         }
     }
     NK(g_nccl.GroupEnd());
@@ -1723,37 +1767,19 @@ static int gp_correct(prs_ctx *ctx) {
                       ctx->gb_d + sl * bvol));
     }
     // gather: U_{n+1} and Gcache_n bands to the owner of slice n, and U_first to this rank
+    TRY(gpar_plan(N, ctx->nranks, me, 1, ops));
     NK(g_nccl.GroupStart());
-    for (int sl = 0; sl < N; ++sl) {
-        const int q = owner(sl);
-        const int qn = (sl + 1 < N) ? owner(sl + 1) : -1;  // U_{sl+1} is also the next owner's input
-        for (int p = 0; p < P; ++p) {
-            // U_{sl+1}: band p -> owner(sl) (end state) and, at a rank edge, -> owner(sl+1)
-            for (int dst : {q, (qn != q) ? qn : -1}) {
-                if (dst < 0) continue;
-                if (p == me && dst == me) {
-                    double *t = (dst == q) ? state(ctx, ctx->traj, sl + 1 - ctx->first) : ctx->traj;
-                    CK(cudaMemcpyAsync(t + p * bvol, ctx->gb_u + (sl + 1) * bvol, bbytes, cudaMemcpyDeviceToDevice,
-                                       ctx->stream));
-                } else if (p == me) {
-                    NK(g_nccl.Send(ctx->gb_u + (sl + 1) * bvol, (size_t)bvol, ncclDouble, dst, ctx->comm,
-                                   ctx->stream));
-                } else if (dst == me) {
-                    double *t = (dst == q) ? state(ctx, ctx->traj, sl + 1 - ctx->first) : ctx->traj;
-                    NK(g_nccl.Recv(t + p * bvol, (size_t)bvol, ncclDouble, p, ctx->comm, ctx->stream));
-                }
-            }
-            // Gcache_sl: band p -> owner(sl)
-            if (p == me && q == me) {
-                CK(cudaMemcpyAsync(state(ctx, ctx->gcache, sl - ctx->first) + p * bvol, ctx->gb_gc + sl * bvol,
-                                   bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
-            } else if (p == me) {
-                NK(g_nccl.Send(ctx->gb_gc + sl * bvol, (size_t)bvol, ncclDouble, q, ctx->comm, ctx->stream));
-            } else if (q == me) {
-                NK(g_nccl.Recv(state(ctx, ctx->gcache, sl - ctx->first) + p * bvol, (size_t)bvol, ncclDouble, p,
-                               ctx->comm, ctx->stream));
-            }
-        }
+    for (size_t o = 0; o < ops.size(); o += 6) {
+        const int kind = ops[o], what = ops[o + 1], sl = ops[o + 2], band = ops[o + 3], peer = ops[o + 4],
+                  lidx = ops[o + 5];
+        double *mine = (what == 1) ? ctx->gb_u + (sl + 1) * bvol : ctx->gb_gc + sl * bvol;  // this rank's band
+        double *dst = ((what == 1) ? state(ctx, ctx->traj, lidx) : state(ctx, ctx->gcache, lidx)) + band * bvol;
+        if (kind == 2)
+            CK(cudaMemcpyAsync(dst, mine, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+        else if (kind == 0)
+            NK(g_nccl.Send(mine, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
+        else
+            NK(g_nccl.Recv(dst, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
     }
     NK(g_nccl.GroupEnd());
     return PRS_OK;
@@ -1914,6 +1940,17 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return PRS_OK;
+}
+
+int prs_gpar_plan(int N, int nranks, int rank, int phase, int *ops, int max_ops) {
+    if (N < 1 || nranks < 1 || rank < 0 || rank >= nranks || (phase != 0 && phase != 1) || max_ops < 0) return -1;
+    std::vector<int> v;
+    if (gpar_plan(N, nranks, rank, phase, v) != PRS_OK) return -1;
+    const int cnt = (int)(v.size() / 6);
+    if (ops)
+        for (int i = 0; i < cnt && i < max_ops; ++i)
+            for (int f = 0; f < 6; ++f) ops[6 * i + f] = v[6 * i + f];
+    return cnt;
 }
 
 int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands) {

@@ -164,3 +164,65 @@ def test_owner_g_schedule_reproduces_serial_parareal(kw):
     assert out[0][2] == out[1][2]
     scale = max(float(np.max(np.abs(t))) for t in trajs)
     assert float(np.max(np.abs(full - trajs[-1]))) / scale <= 1e-14
+
+
+# ------------------------------------------- space-parallel G: band exchange plan
+def _gpar_plan_worker(rank, world, N, L):
+    """Execute this rank's prs_gpar_plan (the ops prs_parareal_correct issues to NCCL) with
+    gloo point-to-point on tagged CPU data; return what landed where."""
+    import paper_2502_08370_b200 as prs
+    P = world
+    first, count = prs.partition(N, P, rank)
+    code = lambda sl, band, kind: float(1000 * sl + 10 * band + kind)  # noqa: E731
+    delta = torch.stack([torch.stack([torch.full((L,), code(first + i, p, 1)) for p in range(P)])
+                         for i in range(count)])
+    traj = torch.full((count + 1, P, L), -1.0)
+    gcache = torch.full((count, P, L), -1.0)
+    gb_d = torch.full((N, L), -1.0)
+    gb_u = torch.stack([torch.full((L,), code(sl, rank, 2)) for sl in range(N + 1)])
+    gb_gc = torch.stack([torch.full((L,), code(sl, rank, 3)) for sl in range(N)])
+    for phase in (0, 1):
+        reqs = []
+        for kind, what, sl, band, peer, lidx in prs.gpar_plan(N, P, rank, phase):
+            if phase == 0:
+                src, dst = (delta[lidx, band] if kind != 1 else None), gb_d[sl]
+            else:
+                src = gb_u[sl + 1] if what == 1 else gb_gc[sl]
+                dst = (traj if what == 1 else gcache)[lidx, band] if kind != 0 else None
+            if kind == 2:
+                dst.copy_(src)
+            elif kind == 0:
+                reqs.append(dist.isend(src.contiguous(), peer))
+            else:
+                buf = torch.empty(L)
+                reqs.append((dist.irecv(buf, peer), buf, dst))
+        for r in reqs:
+            if isinstance(r, tuple):
+                r[0].wait()
+                r[2].copy_(r[1])
+            else:
+                r.wait()
+    return {"first": first, "count": count, "gb_d": gb_d[:, 0].tolist(),
+            "traj": traj[:, :, 0].tolist(), "gcache": gcache[:, :, 0].tolist()}
+
+
+@pytest.mark.parametrize("world,N", [(2, 8), (3, 7), (4, 8)])
+def test_space_parallel_g_exchange_plan(world, N):
+    """SURVEY 8(e) space-parallel G: Delta bands reach their band ranks and every owner gets
+    back all P bands of its U_{n+1}, its incoming U_first and its G cache (the exact op list
+    prs_parareal_correct issues to NCCL, run over gloo)."""
+    import paper_2502_08370_b200 as prs
+    prs.build()  # no-op when libprs.so is current (host logic only: no GPU needed)
+    prs.lib()
+    out = spawn(_gpar_plan_worker, world=world, args=(N, 3))
+    for rank in range(world):
+        o = out[rank]
+        assert not isinstance(o, str), o
+        first, count = o["first"], o["count"]
+        assert o["gb_d"] == [1000.0 * sl + 10 * rank + 1 for sl in range(N)]
+        for i in range(1, count + 1):
+            assert o["traj"][i] == [1000.0 * (first + i) + 10 * p + 2 for p in range(world)]
+        if rank > 0:
+            assert o["traj"][0] == [1000.0 * first + 10 * p + 2 for p in range(world)]
+        for i in range(count):
+            assert o["gcache"][i] == [1000.0 * (first + i) + 10 * p + 3 for p in range(world)]
