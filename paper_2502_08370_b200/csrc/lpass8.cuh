@@ -18,10 +18,17 @@
 
 namespace prs {
 
-constexpr int L8SLOTS = 3;
-constexpr int L8TILE = L5RB * L5W;  // doubles per state tile
+constexpr int L8TILE = L5RB * L5W;     // doubles per state tile
+constexpr int L8SLOT = L8TILE + 2 * L5W;  // + (finish) the tile's y entering / x leaving per column
 
-inline size_t lpass8_smem_bytes() { return sizeof(double) * (size_t)L8SLOTS * L8TILE; }
+// WIDE = 0: 2 CTAs per SM (128 registers), 3-slot ring; WIDE = 1: 1 CTA per SM with the whole
+// register file (no spills of the coefficient registers) and a 4-slot ring
+template <int WIDE>
+struct L8Cfg {
+    static constexpr int SLOTS = WIDE ? 4 : 3;
+    static constexpr int MINB = WIDE ? 1 : 2;
+};
+inline size_t lpass8_smem_bytes(int wide) { return sizeof(double) * (size_t)(wide ? 4 : 3) * L8SLOT; }
 
 // coefficients of one thread's column chunk (rows r0 .. r0+15 of column col)
 template <int COEF>
@@ -51,8 +58,9 @@ __device__ __forceinline__ void l8_load_coef(const L5Args &a, int col, int r0, L
 // MODE 0: block tuples (lp5_tuples_kernel); MODE 1: finish + epilogue (lp5_finish_kernel).
 // Grid: (row block, column block, slice group) with the slice group fastest; a.s8 slices per
 // group.  a.vol is the slice stride.
-template <int COEF, int EPI, int MODE>
-__global__ void __launch_bounds__(L5T, 2) lp8_kernel(L5Args a) {
+template <int COEF, int EPI, int MODE, int WIDE = 0>
+__global__ void __launch_bounds__(L5T, L8Cfg<WIDE>::MINB) lp8_kernel(L5Args a) {
+    constexpr int L8SLOTS = L8Cfg<WIDE>::SLOTS;
     extern __shared__ __align__(16) double ring[];
     __shared__ double st[5][L5CP][L5W];
     const int tid = threadIdx.x;
@@ -71,32 +79,38 @@ __global__ void __launch_bounds__(L5T, 2) lp8_kernel(L5Args a) {
     const long long tile_off = (long long)(rb * L5RB) * n + cb * L5W;
     auto issue = [&](long long b, int slot) {
         const double *src = a.in + b * a.vol + tile_off;
-        double *dst = ring + slot * L8TILE;
+        double *dst = ring + slot * L8SLOT;
 #pragma unroll
         for (int q = 0; q < L8TILE / 2 / L5T; ++q) {  // 8 16-byte pieces per thread
             const int p = tid + q * L5T;
             const int row = p >> 5, u = p & 31;
             cp_async16(dst + row * L5W + 2 * u, src + (long long)row * n + 2 * u);
         }
+        if (MODE == 1 && tid < L5W) {  // the block's boundary values ride along (2 x 64 doubles)
+            const long long ob = (b * a.nrb + rb) * n + cb * L5W;
+            const int h = tid >> 5, u = tid & 31;  // h = 0: y entering, 1: x leaving
+            cp_async16(dst + L8TILE + h * L5W + 2 * u, a.yx + h * a.tstride + ob + 2 * u);
+        }
     };
-    if (b0 < b1) issue(b0, 0);
-    cp_async_commit();
-    if (b0 + 1 < b1) issue(b0 + 1, 1);
-    cp_async_commit();
+#pragma unroll
+    for (int q = 0; q < L8SLOTS - 1; ++q) {
+        if (b0 + q < b1) issue(b0 + q, q);
+        cp_async_commit();
+    }
 
     double dmax = 0.0;
     unsigned long long bad = 0;
     int slot = 0;
     for (long long b = b0; b < b1; ++b) {
         {
-            int s2 = slot + 2;
+            int s2 = slot + L8SLOTS - 1;
             if (s2 >= L8SLOTS) s2 -= L8SLOTS;
-            if (b + 2 < b1) issue(b + 2, s2);
+            if (b + L8SLOTS - 1 < b1) issue(b + L8SLOTS - 1, s2);
             cp_async_commit();
         }
-        cp_async_wait<2>();
+        cp_async_wait<L8SLOTS - 1>();
         __syncthreads();
-        const double *tile = ring + slot * L8TILE;
+        const double *tile = ring + slot * L8SLOT;
 #pragma unroll
         for (int i = 0; i < LCH; ++i) c.v[i] = tile[(t * LCH + i) * L5W + w];
         const Tup u = c.walk1();
@@ -120,8 +134,7 @@ __global__ void __launch_bounds__(L5T, 2) lp8_kernel(L5Args a) {
                 a.tt[4 * a.tstride + o] = tot.R;
             }
         } else {
-            const long long ob = (b * a.nrb + rb) * n + col;
-            const double Yblk = a.yx[ob], Xblk = a.yx[a.tstride + ob];
+            const double Yblk = tile[L8TILE + w], Xblk = tile[L8TILE + L5W + w];
             st[0][t][w] = u.A;
             st[1][t][w] = u.B;
             st[2][t][w] = u.P;

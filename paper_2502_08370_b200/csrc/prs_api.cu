@@ -130,6 +130,8 @@ struct prs_ctx {
     bool no_fused = false;  // PRS_FUSED=0: 2-D long lines take xpass3 + lpass5 (A/B measurements)
     bool fused_notup = false;  // PRS_FUSED=2: xpass6 without the fused y tuples + lp5 tuple kernel
     bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
+    int l8wide = 1;            // lp8 finish at 1 CTA / SM: whole register file (no coefficient spills),
+                               // 4-slot ring; PRS_L8WIDE=0: 2 CTAs / SM, 128 registers, 3 slots
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
     bool x3_contig = false;    // PRS_X3CONTIG=1: xpass3 takes one contiguous range per CTA
     bool no_sweep2 = false;    // PRS_SWEEP2=0: small 2-D slices step through the per-step kernels
@@ -597,6 +599,16 @@ static int launch_lpass3(prs_ctx *ctx, int axis, const TauFactors &f, const doub
 }
 
 // long strided lines (n >= 2048): tuple / scan / finish over 64 x 64 tiles (lpass5.cuh)
+// the lp8 finish instantiation for a coefficient kind, epilogue and register width
+static void (*lp8_finish_fn(int coef, int kind, int wide))(L5Args) {
+    void (*f8)(L5Args) = nullptr;
+#define LK(C, E, W) if (coef == C && kind == E && wide == W) f8 = lp8_kernel<C, E, 1, W>;
+    LK(0, 0, 0) LK(0, 1, 0) LK(0, 2, 0) LK(0, 3, 0) LK(1, 0, 0) LK(1, 1, 0) LK(1, 2, 0) LK(1, 3, 0)
+    LK(0, 0, 1) LK(0, 1, 1) LK(0, 2, 1) LK(0, 3, 1) LK(1, 0, 1) LK(1, 1, 1) LK(1, 2, 1) LK(1, 3, 1)
+#undef LK
+    return f8;
+}
+
 static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out, long long B,
                          const EpiArgs &ep, bool prof) {
     const int n = ctx->p.n, dim = ctx->p.dim;
@@ -654,19 +666,16 @@ static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const doub
         a.s8 = (int)std::min<long long>(B, 16);
         a.nsg8 = (int)((B + a.s8 - 1) / a.s8);
         const long long grid = (long long)a.nrb * a.ncb * a.nsg8;
-        const size_t shm = lpass8_smem_bytes();
+        const size_t shm = lpass8_smem_bytes(0), shmf = lpass8_smem_bytes(ctx->l8wide);
         void (*t8)(L5Args) = coef ? lp8_kernel<1, 0, 0> : lp8_kernel<0, 0, 0>;
-        void (*f8)(L5Args) = nullptr;
-#define LK(C, E) if (coef == C && ep.kind == E) f8 = lp8_kernel<C, E, 1>;
-        LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
-#undef LK
+        void (*f8)(L5Args) = lp8_finish_fn(coef, ep.kind, ctx->l8wide);
         CK(cudaFuncSetAttribute(t8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmf));
         t8<<<(unsigned)grid, L5T, shm, ctx->stream>>>(a);
         TRY(last_launch(ctx));
         lp5_scan_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, ctx->stream>>>(a, ncols);
         TRY(last_launch(ctx));
-        f8<<<(unsigned)grid, L5T, shm, ctx->stream>>>(a);
+        f8<<<(unsigned)grid, L5T, shmf, ctx->stream>>>(a);
         TRY(last_launch(ctx));
     } else {
         k1<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
@@ -997,11 +1006,8 @@ static int launch_tiled2d(prs_ctx *ctx, int scheme, const TauFactors &f, const d
     a.e_red = ctx->red;
     a.s8 = x.s8;
     a.nsg8 = x.nsg8;
-    void (*f8)(L5Args) = nullptr;
-#define LK(C, E) if (coef == C && ep.kind == E) f8 = lp8_kernel<C, E, 1>;
-    LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
-#undef LK
-    const size_t shm8 = lpass8_smem_bytes();
+    void (*f8)(L5Args) = lp8_finish_fn(coef, ep.kind, ctx->l8wide);
+    const size_t shm8 = lpass8_smem_bytes(ctx->l8wide);
     CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm8));
     if (prof) TRY(prof_begin(ctx));
     lp5_scan_kernel<<<(unsigned)((nlines + 255) / 256), 256, 0, ctx->stream>>>(a, nlines);
@@ -1188,6 +1194,8 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         ctx->fused_notup = fv && fv[0] == '2';
         const char *l8 = getenv("PRS_L8");
         ctx->no_l8 = l8 && l8[0] == '0';
+        const char *l8w = getenv("PRS_L8WIDE");
+        ctx->l8wide = (l8w && l8w[0] == '0') ? 0 : 1;
         const char *x7v = getenv("PRS_X7");
         ctx->no_x7 = x7v && x7v[0] == '0';
         const char *xbv = getenv("PRS_X3TMA");

@@ -142,15 +142,18 @@ FUSED_CASES = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["default", "1", "2", "tiled"])
+@pytest.mark.parametrize("mode", ["default", "1", "2", "tiled", "l8narrow"])
 @pytest.mark.parametrize("p", FUSED_CASES, ids=lambda p: p.label())
 def test_fused_long_line_batched_parity(p, mode, monkeypatch):
     """mode: the default long-line path (xpass3 + lp8 tiles persistent over slice groups for
-    n = 2048 / 4096; xpass3 + lpass4 for n = 1024), PRS_FUSED=1 (xpass6 with the y block
-    tuples fused) or 2 (xpass6 + lp5 tuple kernel), or tiled (PRS_TILED=1: lp9 x tiles + lp8,
-    n = 2048 / 4096); the library reads the switches at create."""
+    n = 2048 / 4096, finish at one CTA per SM; xpass3 + lpass4 for n = 1024), PRS_FUSED=1
+    (xpass6 with the y block tuples fused) or 2 (xpass6 + lp5 tuple kernel), tiled
+    (PRS_TILED=1: lp9 x tiles + lp8, n = 2048 / 4096) or l8narrow (PRS_L8WIDE=0: the lp8
+    finish at two CTAs per SM); the library reads the switches at create."""
     if mode == "tiled":
         monkeypatch.setenv("PRS_TILED", "1")
+    elif mode == "l8narrow":
+        monkeypatch.setenv("PRS_L8WIDE", "0")
     elif mode != "default":
         monkeypatch.setenv("PRS_FUSED", mode)
     prs = prs_mod()
