@@ -10,11 +10,14 @@
 // the block solve is exactly (up to rounding)
 //     G = Q^T F  ->  (theta_a I - tau Y) v_a = g_a  (n-long tridiagonal, one per mode a)
 //     ->  U = Q V.
-// One cluster of CL CTAs holds one block of one state in shared memory (R <= 128 rows per
-// CTA): two dense W x W transforms on the fp64 FMA pipes (register-tiled, Q streamed through
-// shared memory), and the n-long tridiagonal solves with the chunk-parallel Thomas of
-// common.cuh across the cluster (distributed shared memory).  This is the fp64-ALU-bound
-// kernel of the path (~4W flops per support point per stage).
+// A block of one state is cut into CL row pieces of R <= 128 rows, one per CTA, each held in
+// shared memory: two dense W x W transforms on the fp64 FMA pipes (register-tiled, Q streamed
+// through shared memory), and the n-long tridiagonal solves with the chunk-parallel Thomas of
+// common.cuh across the pieces.  The pieces exchange their scan totals through L2 (default: a
+// persistent grid taking pieces in order, every SM busy) or through distributed shared memory
+// within a cluster of CL CTAs (PRS_DDCL=1; 8-CTA clusters pack two per GPC, leaving SMs idle).
+// This is the fp64-ALU-bound kernel of the path (~4W flops per support point
+// per stage).
 //
 // FIE step = stage 0 (colour 0) then stage 1 (colour 1), both in place in
 // the output buffer V:
@@ -27,6 +30,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -233,7 +238,29 @@ struct DDStageArgs {
     const double *e_delta;
     double *e_traj;
     unsigned long long *e_red;
+    // global exchange (GX): task counter, per-task flags [2 * ntasks] (forward, backward), per
+    // task scan totals [ntasks][2][DD_WMAX]; zeroed before each launch
+    unsigned *gctr;
+    int *gflag;
+    double2 *gtot;
+    int ntasks;
 };
+
+// L2-scope flag hand-off between CTAs (GX): release after the CTA's total is written, acquire
+// before reading the totals of other row pieces.  A wait that outlives any legitimate one (a
+// task lasts ~0.1 ms) traps instead of hanging the device.
+__device__ __forceinline__ void dd_flag_release(int *f) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(f), "r"(1) : "memory");
+}
+__device__ __forceinline__ void dd_flag_wait(const int *f) {
+    int v;
+    for (long long it = 0;; ++it) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+        if (v) return;
+        if (it > (1ll << 24)) __trap();
+        __nanosleep(32);
+    }
+}
 
 // GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place.
 // 512 threads = 32 row groups x 16 column groups; each thread accumulates 4 rows (rg + 32 r)
@@ -315,20 +342,21 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
     __syncthreads();
 }
 
-template <int DR, int SRC>
-__global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
-    extern __shared__ double sh[];
+// One task: row piece `crank` (of CL) of block `blk` of state `b` (task = b * nblk + blk).
+// GX = 0: the CL pieces are the CTAs of one cluster and exchange their scan totals through
+// distributed shared memory; GX = 1: the pieces are independent tasks of a persistent grid and
+// exchange them through L2 (per-task flags), see dd_stage_kernel.
+template <int DR, int SRC, int GX>
+__device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, long long task, int crank) {
     double *T = sh;                                          // (cpad(R-1)+1) x DD_WPAD
     double *Ms = sh + (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // 2 x DD_KC x DD_WPAD (GEMM)
     double2 *sc = reinterpret_cast<double2 *>(Ms);           // 8 x DD_WMAX chunk maps (y solve)
     double2 *ctf = reinterpret_cast<double2 *>(Ms + 2 * DD_KC * DD_WPAD);  // cluster totals fwd
     double2 *ctb = ctf + DD_WMAX;                             // cluster totals bwd
-    __shared__ double sdmax;
-    __shared__ unsigned long long sbad;
+    const long long tk = task * a.CL + crank;                 // GX slot
+    double2 *gtf = a.gtot + tk * 2 * DD_WMAX, *gtb = gtf + DD_WMAX;
 
     const int tid = threadIdx.x;
-    const int crank = (a.CL > 1) ? (int)cg::this_cluster().block_rank() : 0;
-    const long long task = blockIdx.x / a.CL;
     const int blk = (int)(task % a.nblk);
     const long long b = task / a.nblk;
     const int i0 = a.bi0[blk], W = a.bW[blk];
@@ -338,12 +366,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     const double *Ub = a.U + b * a.vol;
     double *Vb = a.V + b * a.vol;
     const int me = a.stage, other = 1 - a.stage;
-    const double *rn_me = a.rhon + me * n, *rf_me = a.rhof + me * (n + 1);
     const double *rn_ot = a.rhon + other * n, *rf_ot = a.rhof + other * (n + 1);
-    if (tid == 0) {
-        sdmax = 0.0;
-        sbad = 0;
-    }
     double ampt = 0.0;
     if (SRC) ampt = a.src_amp * exp(-src_time(a.ta, b));
 
@@ -475,7 +498,14 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
                 EA = TA;
                 EB = TB;
             }
-            if (t == 0) ctf[am] = make_double2(TA, TB);
+            if (t == 0) {
+                if (GX) {
+                    gtf[am] = make_double2(TA, TB);
+                    __threadfence();
+                } else {
+                    ctf[am] = make_double2(TA, TB);
+                }
+            }
         }
         Ain[rr] = EA;
         Bin[rr] = EB;
@@ -483,7 +513,23 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     double Ycta[NMR];
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) Ycta[rr] = 0.0;
-    if (a.CL > 1) {
+    if (GX && a.CL > 1) {
+        __syncthreads();  // every total of this piece written (and fenced)
+        if (tid == 0) {
+            dd_flag_release(a.gflag + 2 * tk);
+            for (int r = 0; r < crank; ++r) dd_flag_wait(a.gflag + 2 * (task * a.CL + r));
+        }
+        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < NMR; ++rr) {
+            const int am = lane + 32 * (rr0 + rr);
+            if (am < W)
+                for (int r = 0; r < crank; ++r) {
+                    const double2 v = __ldcg(a.gtot + (task * a.CL + r) * 2 * DD_WMAX + am);
+                    Ycta[rr] = fma(v.x, Ycta[rr], v.y);
+                }
+        }
+    } else if (!GX && a.CL > 1) {
         cg::cluster_group cl = cg::this_cluster();
         cl.sync();
 #pragma unroll
@@ -548,7 +594,14 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
                 EP = 1.0;
                 EQ = 0.0;
             }
-            if (t == 0) ctb[am] = make_double2(TP, TQ);
+            if (t == 0) {
+                if (GX) {
+                    gtb[am] = make_double2(TP, TQ);
+                    __threadfence();
+                } else {
+                    ctb[am] = make_double2(TP, TQ);
+                }
+            }
         }
         Ain[rr] = EP;
         Bin[rr] = EQ;
@@ -556,7 +609,23 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
     double Xcta[NMR];
 #pragma unroll
     for (int rr = 0; rr < NMR; ++rr) Xcta[rr] = 0.0;
-    if (a.CL > 1) {
+    if (GX && a.CL > 1) {
+        __syncthreads();
+        if (tid == 0) {
+            dd_flag_release(a.gflag + 2 * tk + 1);
+            for (int r = a.CL - 1; r > crank; --r) dd_flag_wait(a.gflag + 2 * (task * a.CL + r) + 1);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < NMR; ++rr) {
+            const int am = lane + 32 * (rr0 + rr);
+            if (am < W)
+                for (int r = a.CL - 1; r > crank; --r) {
+                    const double2 v = __ldcg(a.gtot + (task * a.CL + r) * 2 * DD_WMAX + DD_WMAX + am);
+                    Xcta[rr] = fma(v.x, Xcta[rr], v.y);
+                }
+        }
+    } else if (!GX && a.CL > 1) {
         cg::cluster_group cl = cg::this_cluster();
         cl.sync();
 #pragma unroll
@@ -652,9 +721,30 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
             if (bad) atomicOr(a.e_red + 1, 1ull);
         }
     }
-    (void)rn_me;
-    (void)rf_me;
-    (void)rf_me;
+}
+
+// GX = 0: one CTA per task piece, clusters of CL CTAs.  GX = 1: a persistent grid (one CTA per
+// SM) whose CTAs take task pieces in order from a global counter; pieces of one block need not
+// be co-resident: a piece waits only on pieces taken before it (forward) or on later pieces of
+// the same block, which the earliest unfinished block always has CTAs free to take, so the
+// in-order hand-out cannot deadlock.  No SM idles for want of a whole free cluster.
+template <int DR, int SRC, int GX>
+__global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
+    extern __shared__ double sh[];
+    if (GX) {
+        __shared__ int s_task;
+        for (;;) {
+            __syncthreads();  // the previous task's last reads of shared memory are done
+            if (threadIdx.x == 0) s_task = (int)atomicAdd(a.gctr, 1u);
+            __syncthreads();
+            const int tk = s_task;
+            if (tk >= a.ntasks) break;
+            dd_stage_task<DR, SRC, 1>(a, sh, tk / a.CL, tk % a.CL);
+        }
+    } else {
+        const int crank = (a.CL > 1) ? (int)cg::this_cluster().block_rank() : 0;
+        dd_stage_task<DR, SRC, 0>(a, sh, blockIdx.x / a.CL, crank);
+    }
 }
 
 inline size_t dd_stage_smem_bytes() {
@@ -676,6 +766,12 @@ struct DDData {
     double tau[3] = {-1.0, -1.0, -1.0};
     std::vector<double *> store[3];
     const double **d_Q[3][2] = {}, **d_QT[3][2] = {}, **d_idy[3][2] = {};
+    // global-exchange stage launch (default; PRS_DDCL=1: clusters)
+    bool gx = true;
+    int num_sms = 148;
+    int *gbuf = nullptr;        // [1 + 2 * gcap]: task counter, flags
+    double2 *gtot = nullptr;    // [gcap][2][DD_WMAX]
+    long long gcap = 0;
 };
 
 // block extents from the index-space geometry (host; integers only, R6)
@@ -737,6 +833,11 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
         cudaMemcpyAsync(d.d_bi0[col], d.bi0[col].data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(d.d_bW[col], d.bW[col].data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st);
     }
+    const char *clv = getenv("PRS_DDCL");
+    d.gx = !(clv && clv[0] == '1');
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaStreamSynchronize(st);
     if (cudaGetLastError() != cudaSuccess) {
         err = "DD table setup failed";
@@ -805,6 +906,8 @@ inline void dd_free(DDData &d) {
         for (double *p : v) cudaFree(p);
         v.clear();
     }
+    if (d.gbuf) cudaFree(d.gbuf);
+    if (d.gtot) cudaFree(d.gtot);
     double *bufs[] = {d.rhon, d.rhof, d.Z};
     for (double *p : bufs)
         if (p) cudaFree(p);
@@ -852,18 +955,35 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
         a.e_delta = delta;
         a.e_traj = traj;
         a.e_red = red;
+        const long long ntasks = B * a.nblk * CL;
+        if (d.gx && ntasks > d.gcap) {
+            if (d.gbuf) cudaFree(d.gbuf);
+            if (d.gtot) cudaFree(d.gtot);
+            d.gbuf = nullptr;
+            d.gtot = nullptr;
+            d.gcap = 0;
+            if (cudaMalloc(&d.gbuf, sizeof(int) * (1 + 2 * ntasks)) != cudaSuccess ||
+                cudaMalloc(&d.gtot, sizeof(double2) * 2 * DD_WMAX * ntasks) != cudaSuccess) {
+                err = "cudaMalloc (DD exchange) failed";
+                return PRS_ECUDA;
+            }
+            d.gcap = ntasks;
+        }
+        a.gctr = reinterpret_cast<unsigned *>(d.gbuf);
+        a.gflag = d.gbuf + 1;
+        a.gtot = d.gtot;
+        a.ntasks = (int)ntasks;
         void (*kern)(DDStageArgs) = nullptr;
         const int dr = scheme == PRS_DR;
-        if (dr && src) kern = dd_stage_kernel<1, 1>;
-        else if (dr) kern = dd_stage_kernel<1, 0>;
-        else if (src) kern = dd_stage_kernel<0, 1>;
-        else kern = dd_stage_kernel<0, 0>;
+#define DK(D, S_, X) if (dr == D && src == S_ && (int)d.gx == X) kern = dd_stage_kernel<D, S_, X>;
+        DK(0, 0, 0) DK(0, 1, 0) DK(1, 0, 0) DK(1, 1, 0) DK(0, 0, 1) DK(0, 1, 1) DK(1, 0, 1) DK(1, 1, 1)
+#undef DK
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess) {
             err = "cudaFuncSetAttribute(dd_stage_kernel) failed";
             return PRS_ECUDA;
         }
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)(B * a.nblk * CL));
+        cfg.gridDim = dim3((unsigned)(d.gx ? std::min<long long>(ntasks, d.num_sms) : ntasks));
         cfg.blockDim = dim3(DD_THREADS);
         cfg.dynamicSmemBytes = shm;
         cfg.stream = st;
@@ -873,7 +993,11 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = d.gx ? 0 : 1;
+        if (d.gx && cudaMemsetAsync(d.gbuf, 0, sizeof(int) * (1 + 2 * ntasks), st) != cudaSuccess) {
+            err = "cudaMemsetAsync (DD exchange flags) failed";
+            return PRS_ECUDA;
+        }
         if (prof && prs_internal_prof_begin(prof) != PRS_OK) return PRS_ECUDA;
         cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
         launches++;

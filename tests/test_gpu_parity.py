@@ -189,10 +189,14 @@ DD_STEP_CASES = [
 ]
 
 
+@pytest.mark.parametrize("exchange", ["l2", "cluster"])
 @pytest.mark.parametrize("p", DD_STEP_CASES, ids=lambda p: f"n{p.n}_S{p.dd_strips}_b{p.dd_overlap}_r{p.dd_ramp}")
-def test_dd_single_step_parity(p):
-    """DD stage solves (separable eigen-transform + cluster tridiagonal) vs the oracle's band
-    elimination, FIE and DR, small and large tau."""
+def test_dd_single_step_parity(p, exchange, monkeypatch):
+    """DD stage solves (separable eigen-transform + row-piece tridiagonal) vs the oracle's band
+    elimination, FIE and DR, small and large tau; row pieces exchanging their scan totals
+    through L2 (default, persistent grid) or within a cluster (PRS_DDCL=1)."""
+    if exchange == "cluster":
+        monkeypatch.setenv("PRS_DDCL", "1")
     prs = prs_mod()
     ctx = prs.Context(p)
     o = oracle.Oracle(p)
