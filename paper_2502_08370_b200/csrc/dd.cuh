@@ -373,6 +373,16 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
     // ---- load the right-hand side tile: one row per warp, columns across lanes; every
     // global load of a row is issued before the first use (several rows' worth in flight) ----
     constexpr int NCW = (DD_WMAX + 31) / 32;  // column slots per lane
+    // per-lane column constants, loaded once: the source profile and, for stage 1, which
+    // columns are already final after stage 0 (rho_0 > 0)
+    unsigned done0m = 0;
+    double spk[NCW];
+#pragma unroll
+    for (int k = 0; k < NCW; ++k) {
+        const int ci = (tid & 31) + 32 * k;
+        spk[k] = (SRC && ci < W) ? __ldg(a.sinpi + i0 + ci) : 0.0;
+        if (me == 1 && ci < W && rn_ot[i0 + ci] > 0.0) done0m |= 1u << k;
+    }
     {
         const int wp = tid >> 5, ln = tid & 31;
         for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
@@ -388,7 +398,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
                     u[k] = in ? Ub[g] : 0.0;
                     r[k] = 0.0;
                 } else {
-                    const bool done0 = in && rn_ot[i0 + ci] > 0.0;  // final after stage 0
+                    const bool done0 = (done0m >> k) & 1u;  // final after stage 0
                     r[k] = done0 ? Vb[g] : 0.0;
                     u[k] = (in && !done0) ? Ub[g] : 0.0;
                 }
@@ -417,13 +427,13 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
                 if (ci < W) {
                     if (me == 0) {
                         v = u[k];
-                        if (SRC) v += sl * a.sinpi[i];
+                        if (SRC) v += sl * spk[k];
                         if (DR) v += wv[k];
-                    } else if (rn_ot[i] > 0.0) {
+                    } else if ((done0m >> k) & 1u) {
                         v = r[k];
                     } else {
                         v = u[k];
-                        if (SRC) v += sl * a.sinpi[i];
+                        if (SRC) v += sl * spk[k];
                     }
                 }
                 if (ci < DD_WMAX) T[cpad(rl) * DD_WPAD + ci] = v;
@@ -670,6 +680,13 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
     double dmax = 0.0;
     unsigned long long bad = 0;
     {
+        // columns whose value is final after this stage (stage 1: all; stage 0: rho_1 = 0)
+        unsigned finm = 0;
+#pragma unroll
+        for (int k = 0; k < NCW; ++k) {
+            const int ci = lane + 32 * k;
+            if (ci < W && (me == 1 || !(rn_ot[i0 + ci] > 0.0))) finm |= 1u << k;
+        }
         const int wp = tid >> 5;
         for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
             const int l = r0 + rl;
@@ -689,7 +706,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
                                       a.h2inv -
                                   rnode * a.c * u);
                 }
-                const bool final_here = (me == 1) || !(rn_ot[i] > 0.0);
+                const bool final_here = (finm >> k) & 1u;
                 const int ep = final_here ? a.epi : EPI_STORE;
                 const long long gb = b * a.vol + g;
                 if (ep == EPI_STORE) {
