@@ -262,12 +262,13 @@ __device__ __forceinline__ void dd_flag_wait(const int *f) {
     }
 }
 
-// GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place.
-// 512 threads = 32 row groups x 16 column groups; each thread accumulates 4 rows (rg + 32 r)
-// x 9 columns (9 cg + j) in registers (36 fp64 FMAs per 13 shared loads per k).  M streams
-// through two shared k-chunks of DD_KC rows with cp.async (next chunk in flight while the
-// current one is consumed).  Columns >= W of T and of the staged M rows are zero, so the
-// inner loops need no predicates; rows >= nrow are computed and discarded.
+// GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place,
+// on the fp64 tensor cores (dd_tile_gemm below).  M streams through two shared k-chunks of
+// DD_KC rows with cp.async (next chunk in flight while the current one is consumed).  Columns
+// >= W of T and of the staged M rows are zero, so the inner loops need no predicates; rows >=
+// nrow are computed and discarded.  (The register-tiled DFMA form reached ~55 % of the fp64
+// pipe: 13 shared loads and 49 issue slots per 36 FMAs; DMMA and DFMA peak alike on B200,
+// profiles/r01_fp64_peak_probe.txt.)
 __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
@@ -287,15 +288,26 @@ __device__ __forceinline__ void dd_stage_mchunk(const double *M, int W, int k0, 
         }
     }
 }
+__device__ __forceinline__ void dmma_f64(double &c0, double &c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
 __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
-    const int tid = threadIdx.x;
-    const int cg = tid & 15, rg = tid >> 4;
-    constexpr int GR = DD_RMAX / (DD_THREADS / 16);  // rows per thread (4)
-    double acc[GR][9];
+    // fp64 tensor-core MMA (m8n8k4): warp w owns rows 16 (w & 7) .. +15 and columns
+    // 72 (w >> 3) .. +71 of the output, i.e. 2 x 9 tiles of 8 x 8, accumulators in registers.
+    // Per 4-wide k step: 2 A fragments (A[r][k], r = lane / 4, k = lane % 4) from the tile and 9
+    // B fragments (B[k][c], k = lane % 4, c = lane / 4) from the staged chunk, all bank-conflict
+    // free with the 148-double row stride; 18 MMAs of 256 FMAs each.
+    static_assert(DD_THREADS == 512 && DD_RMAX == 128 && DD_WMAX == 144 && DD_KC % 4 == 0, "dmma tiling");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rb = 16 * (warp & 7), cb = 72 * (warp >> 3);
+    const int fr = lane >> 2, fk = lane & 3;
+    double acc[2][9][2];
 #pragma unroll
-    for (int r = 0; r < GR; ++r)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int j = 0; j < 9; ++j) acc[r][j] = 0.0;
+        for (int j = 0; j < 9; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
     const int nk = (W + DD_KC - 1) / DD_KC;
     __syncthreads();  // Ms aliases the y-solve scratch: all of its readers are done
     // zero the staged chunks once (columns >= W stay zero; stale rows of a partial last chunk
@@ -304,6 +316,8 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
     __syncthreads();
     dd_stage_mchunk(M, W, 0, Ms);
     cp_async_commit();
+    const double *ta0 = T + cpad(rb + fr) * DD_WPAD + fk;
+    const double *ta1 = T + cpad(rb + 8 + fr) * DD_WPAD + fk;
     for (int kb = 0; kb < nk; ++kb) {
         double *cur = Ms + (kb & 1) * DD_KC * DD_WPAD;
         if (kb + 1 < nk) dd_stage_mchunk(M, W, (kb + 1) * DD_KC, Ms + ((kb + 1) & 1) * DD_KC * DD_WPAD);
@@ -311,31 +325,29 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
         cp_async_wait<1>();
         __syncthreads();
         const int k0 = kb * DD_KC;
-        const double *trow = T + k0;
-        const double *mrow = cur + 9 * cg;
+        const double *tb = cur + fk * DD_WPAD + cb + fr;
 #pragma unroll
-        for (int kk = 0; kk < DD_KC; ++kk) {
-            double f[GR], m[9];
+        for (int kq = 0; kq < DD_KC; kq += 4) {
+            const double a0 = ta0[k0 + kq], a1 = ta1[k0 + kq];
 #pragma unroll
-            for (int r = 0; r < GR; ++r) f[r] = trow[cpad(rg + (DD_THREADS / 16) * r) * DD_WPAD + kk];
-#pragma unroll
-            for (int j = 0; j < 9; ++j) m[j] = mrow[kk * DD_WPAD + j];
-#pragma unroll
-            for (int r = 0; r < GR; ++r)
-#pragma unroll
-                for (int j = 0; j < 9; ++j) acc[r][j] = fma(f[r], m[j], acc[r][j]);
+            for (int j = 0; j < 9; ++j) {
+                const double bv = tb[kq * DD_WPAD + 8 * j];
+                dmma_f64(acc[0][j][0], acc[0][j][1], a0, bv);
+                dmma_f64(acc[1][j][0], acc[1][j][1], a1, bv);
+            }
         }
         __syncthreads();  // chunk consumed before it is refilled
     }
     // all reads of T are done (last barrier above): write in place
 #pragma unroll
-    for (int r = 0; r < GR; ++r) {
-        const int l = rg + (DD_THREADS / 16) * r;
+    for (int h = 0; h < 2; ++h) {
+        const int l = rb + 8 * h + fr;
         if (l < nrow) {
 #pragma unroll
             for (int j = 0; j < 9; ++j) {
-                const int col = 9 * cg + j;
-                if (col < W) T[cpad(l) * DD_WPAD + col] = acc[r][j];
+                const int col = cb + 8 * j + 2 * fk;
+                if (col < W) T[cpad(l) * DD_WPAD + col] = acc[h][j][0];
+                if (col + 1 < W) T[cpad(l) * DD_WPAD + col + 1] = acc[h][j][1];
             }
         }
     }
