@@ -265,8 +265,8 @@ __device__ __forceinline__ void dd_flag_wait(const int *f) {
 // GEMM on the shared tile: T[l][:] <- T[l][:] . M  (M is W x W, row-major, global), in place,
 // on the fp64 tensor cores (dd_tile_gemm below).  M streams through two shared k-chunks of
 // DD_KC rows with cp.async (next chunk in flight while the current one is consumed).  Columns
-// >= W of T and of the staged M rows are zero, so the inner loops need no predicates; rows >=
-// nrow are computed and discarded.  (The register-tiled DFMA form reached ~55 % of the fp64
+// >= W of T and staged rows >= W are zero, so the inner loops need no predicates; rows >= nrow
+// and columns >= W of the product are computed and discarded.  (The register-tiled DFMA form reached ~55 % of the fp64
 // pipe: 13 shared loads and 49 issue slots per 36 FMAs; DMMA and DFMA peak alike on B200,
 // profiles/r01_fp64_peak_probe.txt.)
 __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
@@ -275,16 +275,16 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
 }
 __device__ __forceinline__ void dd_stage_mchunk(const double *M, int W, int k0, double *dst) {
     const int kc = min(DD_KC, W - k0);
-    if ((W & 1) == 0) {  // 16-byte pieces (rows of M are 16-byte aligned)
-        const int pieces = kc * (W / 2);
-        for (int e = threadIdx.x; e < pieces; e += blockDim.x) {
-            const int r = e / (W / 2), h = e - r * (W / 2);
-            cp_async16(dst + r * DD_WPAD + 2 * h, M + (long long)(k0 + r) * W + 2 * h);
+    if ((W & 1) == 0) {  // 16-byte pieces (rows of M are 16-byte aligned), DD_WMAX / 2 slots per row
+        constexpr int PR = DD_WMAX / 2;
+        for (int e = threadIdx.x; e < kc * PR; e += blockDim.x) {
+            const int r = e / PR, h = e - r * PR;
+            if (2 * h < W) cp_async16(dst + r * DD_WPAD + 2 * h, M + (long long)(k0 + r) * W + 2 * h);
         }
     } else {
-        for (int e = threadIdx.x; e < kc * W; e += blockDim.x) {
-            const int r = e / W, c = e - r * W;
-            cp_async8(dst + r * DD_WPAD + c, M + (long long)(k0 + r) * W + c);
+        for (int e = threadIdx.x; e < kc * DD_WMAX; e += blockDim.x) {
+            const int r = e / DD_WMAX, c = e - r * DD_WMAX;
+            if (c < W) cp_async8(dst + r * DD_WPAD + c, M + (long long)(k0 + r) * W + c);
         }
     }
 }
@@ -310,9 +310,16 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
         for (int j = 0; j < 9; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
     const int nk = (W + DD_KC - 1) / DD_KC;
     __syncthreads();  // Ms aliases the y-solve scratch: all of its readers are done
-    // zero the staged chunks once (columns >= W stay zero; stale rows of a partial last chunk
-    // only ever meet the zero columns >= W of T)
-    for (int e = tid; e < 2 * DD_KC * DD_WPAD; e += blockDim.x) Ms[e] = 0.0;
+    // the rows a partial last chunk leaves unwritten meet the zero columns >= W of T and must be
+    // zero (stale scratch need not be finite); staged columns >= W only reach discarded outputs
+    {
+        const int kl = W - (nk - 1) * DD_KC;  // rows of the last chunk
+        double *last = Ms + ((nk - 1) & 1) * DD_KC * DD_WPAD;
+        for (int e = tid; e < (DD_KC - kl) * DD_WMAX; e += blockDim.x) {
+            const int r = e / DD_WMAX;
+            last[(kl + r) * DD_WPAD + (e - r * DD_WMAX)] = 0.0;
+        }
+    }
     __syncthreads();
     dd_stage_mchunk(M, W, 0, Ms);
     cp_async_commit();
@@ -397,6 +404,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
     }
     {
         const int wp = tid >> 5, ln = tid & 31;
+#pragma unroll 2
         for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
             const int l = r0 + rl;
             const long long g0 = (long long)l * n + i0;
