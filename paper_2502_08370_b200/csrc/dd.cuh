@@ -394,16 +394,23 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
     constexpr int NCW = (DD_WMAX + 31) / 32;  // column slots per lane
     // per-lane column constants, loaded once: the source profile and, for stage 1, which
     // columns are already final after stage 0 (rho_0 > 0)
-    unsigned done0m = 0;
+    // finm: columns whose value is final after this stage (stage 1: all; stage 0: rho_1 = 0)
+    unsigned done0m = 0, finm = 0;
     double spk[NCW];
 #pragma unroll
     for (int k = 0; k < NCW; ++k) {
         const int ci = (tid & 31) + 32 * k;
         spk[k] = (SRC && ci < W) ? __ldg(a.sinpi + i0 + ci) : 0.0;
-        if (me == 1 && ci < W && rn_ot[i0 + ci] > 0.0) done0m |= 1u << k;
+        const bool pos = ci < W && rn_ot[i0 + ci] > 0.0;
+        if (me == 1 && pos) done0m |= 1u << k;
+        if (ci < W && (me == 1 || !pos)) finm |= 1u << k;
     }
     {
         const int wp = tid >> 5, ln = tid & 31;
+        // the source profile of the warp's rows wp + 16 q, one per lane (q = lane), shuffled out
+        static_assert(DD_RMAX / (DD_THREADS / 32) <= 32, "rows per warp");
+        double slq = 0.0;
+        if (SRC && wp + (DD_THREADS / 32) * ln < nrow) slq = a.tau * ampt * __ldg(a.sinpi + r0 + wp + (DD_THREADS / 32) * ln);
 #pragma unroll 2
         for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
             const int l = r0 + rl;
@@ -439,7 +446,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
                     }
                 }
             }
-            const double sl = SRC ? a.tau * ampt * a.sinpi[l] : 0.0;
+            const double sl = SRC ? __shfl_sync(0xffffffffu, slq, (rl - wp) / (DD_THREADS / 32)) : 0.0;
 #pragma unroll
             for (int k = 0; k < NCW; ++k) {
                 const int ci = ln + 32 * k, i = i0 + ci;
@@ -700,13 +707,6 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
     double dmax = 0.0;
     unsigned long long bad = 0;
     {
-        // columns whose value is final after this stage (stage 1: all; stage 0: rho_1 = 0)
-        unsigned finm = 0;
-#pragma unroll
-        for (int k = 0; k < NCW; ++k) {
-            const int ci = lane + 32 * k;
-            if (ci < W && (me == 1 || !(rn_ot[i0 + ci] > 0.0))) finm |= 1u << k;
-        }
         const int wp = tid >> 5;
         for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
             const int l = r0 + rl;
