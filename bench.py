@@ -330,8 +330,12 @@ def run_prs(args):
     tr = ncu_traffic(args.config)
     per_launch_s = (kms / nl) / 1e3 if nl else float("nan")
     if dom == prs.PRS_K_DD:
-        # fp64 FMA pipe: 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (B200_PROFILING.md units)
-        peak, peak_src, unit, bound = 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 DFMA/clk x 1.965 GHz", "TFLOP/s", "alu"
+        # the block transforms run on the fp64 tensor cores (DMMA m8n8k4); fp64 peak = 148 SMs x
+        # 64 FP64 FMA/clk x 2 flop x 1.965 GHz = 37.2 TF/s, DMMA and DFMA alike (measured 37.1 /
+        # 35.7 TF/s on this pool's B200, profiles/r01_fp64_peak_probe.txt)
+        peak, peak_src, unit, bound = (148 * 64 * 2 * 1.965e9 / 1e12,
+                                       "derived: 148 SM x 64 fp64 FMA/clk x 1.965 GHz (DMMA measured 37.1 TF/s)",
+                                       "TFLOP/s", "tensor")
         achieved = (kwork / nl) / per_launch_s / 1e12 if nl else 0.0
     else:
         peak, peak_src = measured_peaks()
