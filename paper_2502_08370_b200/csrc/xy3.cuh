@@ -13,8 +13,10 @@
 //    shared memory (chunk-padded: the 8 chunks of a half-warp read 8 different banks);
 //  * y lines cross the two CTAs: each thread walks a 16-row chunk of a column, the 4 chunk
 //    tuples of a CTA are composed through shared memory (lpass4.cuh's 5-tuples), and one
-//    exchange through distributed shared memory gives CTA 1 the y entering its half and CTA 0
-//    the x leaving its half;
+//    exchange gives CTA 1 the y entering its half and CTA 0 the x leaving its half: each CTA
+//    pushes its column totals into the partner's shared memory with st.async, completing on
+//    the partner's mbarrier (no cluster-wide barrier per plane; the only one, split around the
+//    plane load, publishes the mbarrier initialisation);
 //  * the tile uses the chunk-padded row layout (x at x + x/16, row stride 136): the x walks
 //    (rows r, r+1 x 8 chunks per half-warp) and the y walks (consecutive columns) are both
 //    bank-conflict free.
@@ -50,11 +52,19 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
     extern __shared__ __align__(16) double sm[];
     double *tile = sm;                             // 64 x 136
     double *st = tile + XY_R * XY_S;               // [5][4][128] chunk tuples (y)
-    double *ex = st + 5 * 4 * XY_N;                // [3][128] cluster exchange: B (rank 0), Q, R (rank 1)
+    double *ex = st + 5 * 4 * XY_N;                // [3][128]: B of CTA 0's column totals (first row)
     double *ty = ex + 3 * XY_N;                    // [3][136] pivots m, id, cc, chunk-padded (x and y)
+    __shared__ __align__(16) double2 xin[XY_N];  // the partner's column totals
+    __shared__ __align__(8) unsigned long long mbx;
     cg::cluster_group cl = cg::this_cluster();
     const int crank = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&mbx, 1);
+        mbar_fence_init();
+        mbar_arrive_expect(&mbx, XY_N * sizeof(double2));
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     const long long plane = blockIdx.x / 2;
     const long long b = plane / XY_N;
     const int z = (int)(plane - b * XY_N);
@@ -181,29 +191,28 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
         return Tup{st[(0 * 4 + t) * XY_N + w], st[(1 * 4 + t) * XY_N + w], st[(2 * 4 + t) * XY_N + w],
                    st[(3 * 4 + t) * XY_N + w], st[(4 * 4 + t) * XY_N + w]};
     };
-    // CTA totals of the column -> cluster exchange (one thread per column)
+    // CTA totals of the column -> the partner (one thread per column)
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // partner's mbarrier initialised
     if (tid < XY_N) {
         Tup tot = tup_id();
 #pragma unroll
         for (int q = 0; q < 4; ++q) tot = tup_cat(tot, get(q));
         if (crank == 0) {
             ex[w] = tot.B;  // y at this half's last row, from y_in = 0
+            st_async_remote(&xin[w], &mbx, 1, make_double2(tot.B, 0.0));
         } else {
-            ex[XY_N + w] = tot.Q;
-            ex[2 * XY_N + w] = tot.R;
+            st_async_remote(&xin[w], &mbx, 0, make_double2(tot.Q, tot.R));
         }
     }
-    cl.sync();
+    __syncthreads();  // ex[] (CTA 0's own totals) visible to the column's second thread
+    mbar_wait(&mbx, 0);
     double Yin = 0.0, Xout = 0.0;
     if (crank == 0) {
-        const double *pe = cl.map_shared_rank(ex, 1);
-        const double B0 = ex[w];
-        Xout = fma(pe[2 * XY_N + w], B0, pe[XY_N + w]);  // x at row 64: Q1 + R1 y(63)
+        const double2 qr = xin[w];
+        Xout = fma(qr.y, ex[w], qr.x);  // x at row 64: Q1 + R1 y(63)
     } else {
-        const double *pe = cl.map_shared_rank(ex, 0);
-        Yin = pe[w];
+        Yin = xin[w].x;
     }
-    cl.sync();  // the partner's exchange slots are read before either CTA moves on
     auto finish = [&](int t, double (&v)[LCH], const Tup &u) {
         double Y = Yin;
 #pragma unroll

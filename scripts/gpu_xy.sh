@@ -1,3 +1,2 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "xy_fused or 3d or c2 or dim_FIE or graph or fine_solve" > gpurun_out/pytest_xy.log 2>&1; echo "pytest rc=$?"
-python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2_xy.json 2> gpurun_out/bench_c2_xy.err; echo "bench rc=$?"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"xy3|lpass3" --launch-skip 200 -c 4 --csv python bench.py --config c2 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 --no-time-to-tol > gpurun_out/ncu_xy.csv 2> gpurun_out/ncu_xy.err; echo "ncu rc=$?"
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "c2 or xy or 128" > gpurun_out/pytest_xy.log 2>&1; echo "pytest rc=$?"
+timeout 300 python bench.py --config c2 --no-cpu-baseline --no-time-to-tol --e2e-steps 0 > gpurun_out/bench_c2_msg.json 2> gpurun_out/bench_c2.err; echo "bench rc=$?"
