@@ -199,6 +199,16 @@ __device__ __forceinline__ void st_async_remote(double2 *dst, unsigned long long
                  : "memory");
 }
 
+// the same for one double (8 bytes)
+__device__ __forceinline__ void st_async_remote_f64(double *dst, unsigned long long *mb, unsigned rank, double v) {
+    unsigned rd, rm;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rd) : "r"(smem_u32(dst)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rm) : "r"(smem_u32(mb)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(rd), "d"(v),
+                 "r"(rm)
+                 : "memory");
+}
+
 // Walk dispatch: `full` must be uniform over the CTA (every chunk of every line has LCH
 // elements, or the predicated variant runs).
 template <class V>

@@ -53,7 +53,7 @@ constexpr bool sweep2_own_column() { return N == SW_T; }
 template <int N>
 constexpr size_t sweep2_smem_doubles() {
     return (size_t)SW_R * (N + N / LCH) + 3 * (N + N / LCH) + (sweep2_own_column<N>() ? 0 : 5 * 2 * N + 2 * N) +
-           5 * N + 2 * 2 * (N + N / LCH);
+           2 * 5 * N + 2 * 2 * (N + N / LCH);
 }
 
 template <int N, int DR, int SRC, int EPI, int CHAIN = 0>
@@ -67,17 +67,26 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
     double *tile = sm;                          // 32 x S
     double *tb = tile + SW_R * S;               // [3][S] m, id, cc (chunk-padded)
     constexpr bool OWN = sweep2_own_column<N>();
-    double *ctot = tb + 3 * S;                  // [5][N] this CTA's column totals (read remotely)
-    double *edge = ctot + 5 * N;                // [parity][2][S] copies of the first / last row (DR halo
-                                                // for the neighbours, published at the end of each step)
-    double *chk = edge + 2 * 2 * S;             // (!OWN) [5][2][N] chunk tuples (y)
+    double *ctot0 = tb + 3 * S;                 // [parity][5][N] this CTA's column totals (read remotely)
+    double *ein = ctot0 + 2 * 5 * N;            // [parity][2][S] the neighbours' edge rows (DR halo): [0] the
+                                                // row above this CTA's first, [1] the row below its last
+    double *chk = ein + 2 * 2 * S;              // (!OWN) [5][2][N] chunk tuples (y)
     double *yxb = chk + 5 * 2 * N;              // (!OWN) [2][N] y entering / x leaving this CTA
+    __shared__ __align__(8) unsigned long long mbe;  // edge rows received (DR)
     cg::cluster_group cl = cg::this_cluster();
     const int crank = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31;
     const long long b = blockIdx.x / CL;
     const int r0 = crank * SW_R;  // first global row of this CTA
     const long long base = b * a.vol + (long long)r0 * N;
+    constexpr bool HALO = DR && CL > 1;
+    const unsigned ebytes = (unsigned)(((crank > 0) + (crank < CL - 1)) * N * sizeof(double));
+    if (HALO && tid == 0) {
+        mbar_init(&mbe, 1);
+        mbar_fence_init();
+        mbar_arrive_expect(&mbe, ebytes);  // step 0's halo rows
+    }
+    if (HALO) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 
     for (int e = tid; e < N; e += SW_T) {
         tb[cpad(e)] = __ldg(a.tab.m + e);
@@ -91,19 +100,20 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
         d[0] = v.x;
         d[1] = v.y;
     }
-    // neighbour CTAs' published edge rows (DR halo rows)
-    const double *edge_up = (crank > 0) ? cl.map_shared_rank(edge, crank - 1) : nullptr;
-    const double *edge_dn = (crank < CL - 1) ? cl.map_shared_rank(edge, crank + 1) : nullptr;
-    auto publish_edges = [&](int par) {  // rows 0 and 31 of the tile -> edge[par]
-        double *e = edge + par * 2 * S;
-        for (int x = tid; x < S; x += SW_T) {
-            e[x] = tile[x];
-            e[S + x] = tile[(SW_R - 1) * S + x];
+    // DR halo: this CTA's first row goes to the CTA above (its "row below"), its last row to
+    // the CTA below (its "row above"), pushed with st.async into the receiver's parity slot and
+    // completing on the receiver's mbarrier; a CTA waits only for its two neighbours
+    auto send_edges = [&](int par) {
+        for (int e = tid; e < N; e += SW_T) {  // (chunk-padded offsets: 8-byte messages)
+            const int x = cpad(e);
+            if (crank > 0) st_async_remote_f64(ein + par * 2 * S + S + x, &mbe, crank - 1, tile[x]);
+            if (crank < CL - 1) st_async_remote_f64(ein + par * 2 * S + x, &mbe, crank + 1, tile[(SW_R - 1) * S + x]);
         }
     };
-    if (DR) {
-        __syncthreads();  // the whole tile is loaded
-        publish_edges(0);
+    __syncthreads();  // the whole tile is loaded
+    if (HALO) {
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // neighbours' mbarriers initialised
+        send_edges(0);
     }
     const double tauh = a.tau * a.h2inv, taucr = a.tau * a.creact;
     constexpr int NXT = (XT + SW_T - 1) / SW_T, NYT = (YT + SW_T - 1) / SW_T;
@@ -111,8 +121,14 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
     unsigned long long cbad = 0;
 
     for (int j = 0; j < a.s; ++j) {
-        cl.sync();  // previous step complete in every CTA (edge rows published, remote totals consumed)
+        // (no cluster barrier here: the column totals are double-buffered by step parity, and
+        // the halo rows arrive as messages)
         const int par = j & 1;
+        double *ctot = ctot0 + par * 5 * N;
+        if (HALO) {
+            mbar_wait(&mbe, (unsigned)par);  // this step's halo rows have landed
+            if (tid == 0 && j + 1 < a.s) mbar_arrive_expect(&mbe, ebytes);  // arm the next step's
+        }
         // ---------------- x stage ----------------
         // (a) w = tau A_y U of every task (reads rows r-1, r+1, the neighbour CTAs' edge rows)
         double w[NXT][LCH];
@@ -122,10 +138,10 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
             if (!DR || q >= XT) break;
             const int r = q / CH, c = q % CH;
             const double *p = tile + r * S + c * LCP;
-            // the neighbours' edge rows come from their published copies (parity of this step),
-            // so the in-place solve below needs no cluster barrier before it
-            const double *pm = (r > 0) ? p - S : (edge_up ? edge_up + par * 2 * S + S + c * LCP : nullptr);
-            const double *pp = (r < SW_R - 1) ? p + S : (edge_dn ? edge_dn + par * 2 * S + c * LCP : nullptr);
+            // the neighbours' edge rows are local copies (parity of this step), so the in-place
+            // solve below needs no cluster barrier before it
+            const double *pm = (r > 0) ? p - S : (crank > 0 ? ein + par * 2 * S + c * LCP : nullptr);
+            const double *pp = (r < SW_R - 1) ? p + S : (crank < CL - 1 ? ein + par * 2 * S + S + c * LCP : nullptr);
 #pragma unroll
             for (int i = 0; i < LCH; ++i) {
                 const double uu = p[i];
@@ -309,9 +325,9 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
             }
             __syncthreads();
         }
-        // publish this step's edge rows into the other parity (read by the neighbours in step
-        // j+1, after its first cluster barrier; the parity read in step j is not touched)
-        if (DR) publish_edges(par ^ 1);
+        // this step's edge rows into the neighbours' other parity slot (read in step j + 1; the
+        // slot read in step j is not touched)
+        if (HALO && j + 1 < a.s) send_edges(par ^ 1);
     }
     cl.sync();  // no CTA leaves while a neighbour may still read its shared memory
     if (CHAIN) {
