@@ -48,6 +48,10 @@ def parse():
                     help="coarse chain: owner-G (default) or space-parallel G over P row bands "
                          "(P = GPUs; --gbands virtual bands on one GPU)")
     ap.add_argument("--gbands", type=int, default=4)
+    ap.add_argument("--pipeline", type=int, default=0, metavar="BLOCKS",
+                    help="pipelined parareal (prs_set_pipeline, NEXT-2): the timed steps and the "
+                         "time-to-tol run as one prs_iterate over BLOCKS slice blocks (on-chip "
+                         "sweep configs c0/c1/c1p; 0 = off)")
     ap.add_argument("--no-time-to-tol", action="store_true",
                     help="skip the parareal time-to-tolerance run and the sequential fine solve")
     return ap.parse_args()
@@ -217,6 +221,8 @@ def run_prs(args):
     ctx = prs.Context(p, rank=rank, nranks=world, nccl_uid=uid, stream=stream.cuda_stream)
     if args.coarse_mode == "space":
         ctx.set_coarse_mode(1, world if world > 1 else args.gbands)
+    if args.pipeline:
+        ctx.set_pipeline(args.pipeline)
     u0 = synth.initial_state(p)
     u0_host = torch.from_numpy(u0).pin_memory()
     u0_dev = u0_host.cuda()
@@ -232,8 +238,11 @@ def run_prs(args):
         ctx.fine_sweep()
         return ctx.parareal_correct()
 
-    for _ in range(args.warmup):
-        step()
+    if args.pipeline:  # K pipelined iterations per call (no stop test: tol = 0)
+        ctx.iterate(max(1, min(args.warmup, p.N)), 0.0)
+    else:
+        for _ in range(args.warmup):
+            step()
     barrier()
     # timed region: the production path (CUDA-graph replays on one rank), no per-kernel events
     clocks = ClockSampler(local)
@@ -243,8 +252,12 @@ def run_prs(args):
     barrier()
     ev0.record(stream)
     upds = []
-    for _ in range(args.steps):
-        upds.append(step())
+    if args.pipeline:
+        assert args.steps <= p.N, "--pipeline: steps <= N (one prs_iterate call)"
+        _, upds = ctx.iterate(args.steps, 0.0)
+    else:
+        for _ in range(args.steps):
+            upds.append(step())
     ev1.record(stream)
     torch.cuda.synchronize()
     launches = ctx.launches() - l0
@@ -368,7 +381,7 @@ def run_prs(args):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": workload_config(p, args.config, world),
                 "parallelism": f"time-slices x{world}",
-                "coarse_mode": args.coarse_mode,
+                "coarse_mode": args.coarse_mode, "pipeline_blocks": args.pipeline,
                 "updates": upds, "gpu_launches": launches, "clocks": clk, "roofline": roof,
                 "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt}
         print(json.dumps(line), flush=True)

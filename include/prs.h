@@ -129,6 +129,19 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
  *   n % (64 P) == 0 (PRS_EUNSUPPORTED otherwise).  Results equal owner-G up to rounding. */
 int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands);
 
+/* Pipelined parareal for prs_iterate: blocks > 0 cuts
+ * the local slices into `blocks` blocks and runs each iteration as a per-block dependency
+ * graph on CUDA streams: the fine sweep of block b in iteration k+1 starts as soon as the
+ * coarse chain of iteration k has corrected block b (F on slice n needs only U^{k+1}_n), and
+ * the chain of iteration k+1 follows the fine sweeps block by block.  The stop test of
+ * iteration k is read while iteration k+1 already runs (one iteration of lookahead, on the
+ * other parity of a double-buffered trajectory / G cache, drained and discarded on stop), so
+ * results -- trajectory, k, update history -- are bitwise those of the unpipelined path.
+ * blocks = 0 turns it off.  Supported for one rank on the on-chip sweep path (2-D dimensional
+ * split, kappa = 1, n in {32, 64, 128, 256}, owner-G); PRS_EUNSUPPORTED otherwise.  Allocates
+ * a second trajectory and G cache.  Only prs_iterate is pipelined. */
+int prs_set_pipeline(prs_ctx *ctx, int blocks);
+
 /* Host only (no GPU): the band exchange of space-parallel G for `rank` of nranks and N slices,
  * phase 0 (scatter of Delta bands from the slice owners) or 1 (gather of U / G-cache bands back
  * to them), as the point-to-point operations prs_parareal_correct issues (NCCL group).  Writes

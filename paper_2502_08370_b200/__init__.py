@@ -20,7 +20,7 @@ PRS_FIE, PRS_DR = 0, 1
 PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
 EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
-           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_gpar_plan", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
+           "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_set_pipeline", "prs_gpar_plan", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
            "prs_last_error", "prs_destroy"]
 
 
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
             "prs_step_batch": ([V, I, I, I, V, V, I], I),
             "prs_fine_solve": ([V, V, I, I, V, I], I),
             "prs_set_coarse_mode": ([V, I, I], I),
+            "prs_set_pipeline": ([V, I], I),
             "prs_gpar_plan": ([I, I, I, I, PI, I], I),
             "prs_set_profiling": ([V, I], I),
             "prs_launches": ([V], ctypes.c_longlong),
@@ -207,6 +208,10 @@ class Context:
         """0: owner-G chain; 1: space-parallel G over P row bands (P = nranks, or `bands`
         virtual bands on one rank)."""
         self._check(self.L.prs_set_coarse_mode(self.h, mode, bands))
+
+    def set_pipeline(self, blocks: int):
+        """Pipelined parareal for iterate(): `blocks` slice blocks (0: off)."""
+        self._check(self.L.prs_set_pipeline(self.h, blocks))
 
     def set_profiling(self, on: bool):
         self._check(self.L.prs_set_profiling(self.h, int(on)))

@@ -168,6 +168,16 @@ struct prs_ctx {
     double *gb_yx = nullptr;   // per band: y entering / x leaving [P][2][n]
     double *l5buf = nullptr;  // lpass5 block tuples and block y/x
     size_t l5_bytes = 0;
+    // pipelined parareal (prs_set_pipeline): the local slices in `pipe`
+    // blocks; trajectory and G cache double-buffered by iteration parity (traj2, gcache2)
+    int pipe = 0;
+    double *traj2 = nullptr, *gcache2 = nullptr;
+    cudaStream_t psC = nullptr;              // the coarse chain
+    std::vector<cudaStream_t> psF;           // fine sweep of block b
+    std::vector<cudaEvent_t> pevF, pevC;     // block b: fine sweep done / chain done
+    cudaEvent_t pev0 = nullptr, pevRed[2] = {nullptr, nullptr};
+    unsigned long long *pred = nullptr;      // [parity][2] update bits, non-finite flag
+    unsigned long long *pred_host = nullptr; // pinned copy
     std::string err;
 };
 
@@ -1286,6 +1296,33 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
     return PRS_OK;
 }
 
+static void pipe_free(prs_ctx *ctx) {
+    for (auto st : ctx->psF) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    if (ctx->psC) {
+        cudaStreamSynchronize(ctx->psC);
+        cudaStreamDestroy(ctx->psC);
+    }
+    for (auto e : ctx->pevF) cudaEventDestroy(e);
+    for (auto e : ctx->pevC) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ctx->pev0, ctx->pevRed[0], ctx->pevRed[1]})
+        if (e) cudaEventDestroy(e);
+    if (ctx->traj2) cudaFree(ctx->traj2);
+    if (ctx->gcache2) cudaFree(ctx->gcache2);
+    if (ctx->pred) cudaFree(ctx->pred);
+    if (ctx->pred_host) cudaFreeHost(ctx->pred_host);
+    ctx->psF.clear();
+    ctx->pevF.clear();
+    ctx->pevC.clear();
+    ctx->psC = nullptr;
+    ctx->pev0 = ctx->pevRed[0] = ctx->pevRed[1] = nullptr;
+    ctx->traj2 = ctx->gcache2 = nullptr;
+    ctx->pred = ctx->pred_host = nullptr;
+    ctx->pipe = 0;
+}
+
 void prs_destroy(prs_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
@@ -1316,6 +1353,7 @@ void prs_destroy(prs_ctx *ctx) {
     }
     if (ctx->corr_exec) cudaGraphExecDestroy(ctx->corr_exec);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    pipe_free(ctx);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1389,7 +1427,7 @@ static bool sweep2_ok(const prs_ctx *ctx) {
 }
 
 static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const double *gc, long long B, long long slice0,
-                         int steps) {
+                         int steps, cudaStream_t st = nullptr) {
     const int n = ctx->p.n;
     const TauFactors &f = ctx->fac[1];
     SWArgs a{};
@@ -1425,7 +1463,7 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
     cfg.gridDim = dim3((unsigned)(B * CL));
     cfg.blockDim = dim3(SW_T);
     cfg.dynamicSmemBytes = shm;
-    cfg.stream = ctx->stream;
+    cfg.stream = st ? st : ctx->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
@@ -1441,17 +1479,20 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
     return PRS_OK;
 }
 
-// the coarse chain of local slices i0 .. count-1 on chip (sweep2 with CHAIN = 1): one cluster
-static int launch_chain2(prs_ctx *ctx, int i0, int epi) {
-    const int n = ctx->p.n, cnt = ctx->count - i0;
+// the coarse chain of local slices i0 .. i1-1 on chip (sweep2 with CHAIN = 1): one cluster.
+// traj / gcache / delta are batch buffers (slice stride ss); U_{i0} is read from traj.
+static int launch_chain2x(prs_ctx *ctx, double *traj, double *gcache, const double *delta, int i0, int i1, int epi,
+                          unsigned long long *red, cudaStream_t st, const double *trajold = nullptr) {
+    const int n = ctx->p.n, cnt = i1 - i0;
     if (cnt <= 0) return PRS_OK;
     const TauFactors &f = ctx->fac[0];
     SWArgs a{};
-    a.in = state(ctx, ctx->traj, i0);
-    a.traj = state(ctx, ctx->traj, i0);
-    a.gcache = state(ctx, ctx->gcache, i0);
-    a.delta = (epi == EPI_CORRECT) ? state(ctx, ctx->delta, i0) : nullptr;
-    a.red = ctx->red;
+    a.in = state(ctx, traj, i0);
+    a.traj = state(ctx, traj, i0);
+    a.trajold = trajold ? state(ctx, const_cast<double *>(trajold), i0) : nullptr;
+    a.gcache = state(ctx, gcache, i0);
+    a.delta = (epi == EPI_CORRECT) ? state(ctx, const_cast<double *>(delta), i0) : nullptr;
+    a.red = red;
     a.vol = ctx->ss;
     a.s = cnt;
     a.tau = f.tau;
@@ -1486,7 +1527,7 @@ static int launch_chain2(prs_ctx *ctx, int i0, int epi) {
     cfg.gridDim = dim3((unsigned)CL);
     cfg.blockDim = dim3(SW_T);
     cfg.dynamicSmemBytes = shm;
-    cfg.stream = ctx->stream;
+    cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
@@ -1496,6 +1537,10 @@ static int launch_chain2(prs_ctx *ctx, int i0, int epi) {
     cfg.numAttrs = 1;
     CK(cudaLaunchKernelEx(&cfg, k, a));
     return last_launch(ctx);
+}
+
+static int launch_chain2(prs_ctx *ctx, int i0, int epi) {
+    return launch_chain2x(ctx, ctx->traj, ctx->gcache, ctx->delta, i0, ctx->count, epi, ctx->red, ctx->stream);
 }
 
 static int enqueue_fine_sweep(prs_ctx *ctx) {
@@ -1852,8 +1897,126 @@ int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
     return PRS_OK;
 }
 
+// ---------------------------------------------------------- pipelined parareal -------
+// Iteration k (U^k -> U^{k+1}) as a per-block dependency graph on streams:
+//   fine(k, b)  : Delta_i = F^s(U^k_i) - G(U^k_i) for the slices of block b (sweep2), once the
+//                 chain of iteration k-1 has produced U^k and G(U^k) of that block;
+//   chain(k, b) : G step + fused correction of block b's slices, in time order, once fine(k, b)
+//                 is done and chain(k, b-1) has produced U^{k+1} of the block's first slice.
+// So the fine sweeps of iteration k+1 start block by block while the chain of iteration k is
+// still correcting later blocks, and the chain of k+1 follows the fine sweeps as they land
+// (F on slice n needs only U^{k+1}_n).  Iteration k reads the parity-(k & 1)
+// trajectory / G cache and writes the other parity, so an iteration started before the stop
+// test of the previous one (one iteration of lookahead) never touches the converged iterate;
+// it is drained and discarded.  The kernels and their inputs are those of the unpipelined
+// path, so trajectories and update histories are bitwise identical to it.
+static int pipe_enqueue(prs_ctx *ctx, int k) {
+    const int G = ctx->pipe, cnt = ctx->count, s = ctx->p.s, p = k & 1, q = p ^ 1;
+    double *T[2] = {ctx->traj, ctx->traj2}, *GC[2] = {ctx->gcache, ctx->gcache2};
+    double *D = ctx->fa;
+    for (int b = 0; b < G; ++b) {
+        const int lo = (int)((long long)b * cnt / G), hi = (int)((long long)(b + 1) * cnt / G);
+        if (k > 0) CK(cudaStreamWaitEvent(ctx->psF[b], ctx->pevC[b], 0));
+        if (hi > lo)
+            TRY(launch_sweep2(ctx, state(ctx, T[p], lo), state(ctx, D, lo), state(ctx, GC[p], lo), hi - lo,
+                              ctx->first + lo, s, ctx->psF[b]));
+        CK(cudaEventRecord(ctx->pevF[b], ctx->psF[b]));
+    }
+    CK(cudaMemsetAsync(ctx->pred + 2 * p, 0, 2 * sizeof(unsigned long long), ctx->psC));
+    for (int b = 0; b < G; ++b) {
+        const int lo = (int)((long long)b * cnt / G), hi = (int)((long long)(b + 1) * cnt / G);
+        CK(cudaStreamWaitEvent(ctx->psC, ctx->pevF[b], 0));
+        TRY(launch_chain2x(ctx, T[q], GC[q], D, lo, hi, EPI_CORRECT, ctx->pred + 2 * p, ctx->psC, T[p]));
+        CK(cudaEventRecord(ctx->pevC[b], ctx->psC));
+    }
+    CK(cudaMemcpyAsync(ctx->pred_host + 2 * p, ctx->pred + 2 * p, 2 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, ctx->psC));
+    CK(cudaEventRecord(ctx->pevRed[p], ctx->psC));
+    return PRS_OK;
+}
+
+static int pipe_iterate(prs_ctx *ctx, int K, double tol, int *k_out, double *hist) {
+    TRY(ensure_factors(ctx, 0, ctx->dT));
+    TRY(ensure_factors(ctx, 1, ctx->dt));
+    // parity 1 starts from the same U_0 (slice 0 of every iterate)
+    CK(cudaMemcpyAsync(ctx->traj2, ctx->traj, ctx->sbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->pev0, ctx->stream));
+    for (auto st : ctx->psF) CK(cudaStreamWaitEvent(st, ctx->pev0, 0));
+    CK(cudaStreamWaitEvent(ctx->psC, ctx->pev0, 0));
+    int k = 0, rc = PRS_OK;
+    if (K > 0) rc = pipe_enqueue(ctx, 0);
+    while (rc == PRS_OK && k < K) {
+        if (k + 1 < K) {
+            rc = pipe_enqueue(ctx, k + 1);  // lookahead: runs while iteration k's chain finishes
+            if (rc != PRS_OK) break;
+        }
+        const int p = k & 1;
+        CK(cudaEventSynchronize(ctx->pevRed[p]));
+        double upd;
+        memcpy(&upd, ctx->pred_host + 2 * p, sizeof(double));
+        const bool bad = ctx->pred_host[2 * p + 1] != 0;
+        upd /= ctx->u0norm;
+        if (hist) hist[k] = upd;
+        ++k;
+        if (bad) {
+            ctx->err = "non-finite value in the parareal iterate";
+            rc = PRS_EDIVERGED;
+            break;
+        }
+        if (upd <= tol) break;
+    }
+    // drain the lookahead iteration (it wrote only the other parity and the Delta scratch)
+    for (auto st : ctx->psF) CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(ctx->psC));
+    if (k & 1) {  // U^k and G(U^k) are in parity 1: make parity 0 (ctx->traj / gcache) current
+        CK(cudaMemcpyAsync(ctx->traj, ctx->traj2, ctx->ss * sizeof(double) * (size_t)(ctx->count + 1),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->gcache, ctx->gcache2, ctx->ss * sizeof(double) * (size_t)ctx->count,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->delta = nullptr;
+    if (k_out) *k_out = k;
+    return rc;
+}
+
+int prs_set_pipeline(prs_ctx *ctx, int blocks) {
+    if (!ctx || blocks < 0) return PRS_EINVAL;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    pipe_free(ctx);
+    if (blocks == 0) return PRS_OK;
+    if (ctx->nranks != 1 || !sweep2_ok(ctx) || ctx->gpar) {
+        ctx->err = "pipelined parareal: one rank, 2-D dimensional split with kappa = 1 and n in {32, 64, 128, 256} "
+                   "(the on-chip sweep kernels), owner-G coarse mode";
+        return PRS_EUNSUPPORTED;
+    }
+    const int G = blocks < ctx->count ? blocks : ctx->count;
+    CK(cudaMalloc(&ctx->traj2, ctx->ss * sizeof(double) * (size_t)(ctx->count + 1)));
+    CK(cudaMalloc(&ctx->gcache2, ctx->ss * sizeof(double) * (size_t)ctx->count));
+    CK(cudaMalloc(&ctx->pred, 4 * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&ctx->pred_host, 4 * sizeof(unsigned long long)));
+    ctx->psF.resize(G);
+    ctx->pevF.resize(G);
+    ctx->pevC.resize(G);
+    for (int b = 0; b < G; ++b) {
+        CK(cudaStreamCreateWithFlags(&ctx->psF[b], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->pevF[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->pevC[b], cudaEventDisableTiming));
+    }
+    CK(cudaStreamCreateWithFlags(&ctx->psC, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->pev0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->pevRed[0], cudaEventDisableTiming | cudaEventBlockingSync));
+    CK(cudaEventCreateWithFlags(&ctx->pevRed[1], cudaEventDisableTiming | cudaEventBlockingSync));
+    ctx->pipe = G;
+    return PRS_OK;
+}
+
 int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
     if (!ctx || kmax < 0) return PRS_EINVAL;
+    if (ctx->pipe) {
+        if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
+        return pipe_iterate(ctx, kmax < ctx->p.N ? kmax : ctx->p.N, tol, k_out, hist);
+    }
     const int K = kmax < ctx->p.N ? kmax : ctx->p.N;
     int k = 0;
     int rc = PRS_OK;

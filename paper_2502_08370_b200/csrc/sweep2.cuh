@@ -34,6 +34,8 @@ struct SWArgs {
     // coarse chain (CHAIN = 1): one cluster runs the s G steps of slices i0 .. i0+s-1 in turn,
     // U_{i+1} <- G(U_i) (+ Delta_i, EPI_CORRECT), the G cache of slice i <- G(U_i)
     double *traj;         // U_i of local slice i at traj + i vol
+    const double *trajold;  // U^k_i for the update norm when it is not in traj (pipelined
+                            // parareal: the previous iterate lives in the other parity buffer)
     double *gcache;
     const double *delta;
     unsigned long long *red;  // [0] max |update| bits, [1] non-finite flag (EPI_CORRECT)
@@ -313,7 +315,8 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
                 double2 nv = gv;
                 if (EPI == EPI_CORRECT) {
                     const double2 dv = *reinterpret_cast<const double2 *>(a.delta + (long long)j * a.vol + off);
-                    const double2 ov = *reinterpret_cast<const double2 *>(a.traj + (long long)(j + 1) * a.vol + off);
+                    const double2 ov = *reinterpret_cast<const double2 *>((a.trajold ? a.trajold : a.traj) +
+                                                                         (long long)(j + 1) * a.vol + off);
                     nv.x += dv.x;
                     nv.y += dv.y;
                     cdmax = fmax(cdmax, fmax(fabs(nv.x - ov.x), fabs(nv.y - ov.y)));

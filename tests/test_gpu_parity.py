@@ -562,6 +562,62 @@ def test_iterate_skipping_converged_slices_is_bitwise_neutral(p, monkeypatch):
         assert float(np.max(np.abs(outs[0][2] - fine))) / scale <= TOL
 
 
+PIPE_CASES = [
+    (Problem(dim=2, n=32, c=1.0, source=1, N=8, s=4, G=FIE, F=FIE), 3, 0.0),
+    (Problem(dim=2, n=64, c=2.0, source=1, N=7, s=3, G=FIE, F=DR), 7, 0.0),
+    (Problem(dim=2, n=256, c=1.0, N=12, s=8, G=FIE, F=DR, init="modes", seed=3), 4, 1e-6),
+    (Problem(dim=2, n=128, c=1.0, source=1, N=9, s=2, G=DR, F=FIE), 2, 1e-4),
+    (Problem(dim=2, n=256, c=1.0, N=5, s=4, G=DR, F=DR), 1, 0.0),
+]
+
+
+@pytest.mark.parametrize("p,blocks,tol", PIPE_CASES, ids=lambda x: x.label() if hasattr(x, "label") else str(x))
+def test_pipelined_iterate_is_bitwise_the_unpipelined_one(p, blocks, tol):
+    """NEXT-2 pipelined parareal (prs_set_pipeline): per-block fine sweeps of iteration k+1
+    overlapping the coarse chain of iteration k, one iteration of lookahead past the stop test.
+    Same kernels and inputs, so k, the update history and the whole trajectory equal the
+    unpipelined prs_iterate bit for bit -- also when tol stops it early (the lookahead iteration
+    is discarded) -- and the iteration can continue afterwards from the same state."""
+    prs = prs_mod()
+    u0 = synth.initial_state(p) + 1e-3 * rand_field(p, 77)
+    outs = []
+    for blk in (blocks, 0):
+        ctx = prs.Context(p)
+        ctx.set_pipeline(blk)
+        ctx.set_initial(dev(u0))
+        ctx.coarse_sweep()
+        k, hist = ctx.iterate(p.N, tol)
+        buf = torch.empty((p.n,) * p.dim, dtype=torch.float64, device="cuda")
+        traj = np.stack([host(ctx.get_slice(n, buf)).copy() for n in range(p.N + 1)])
+        # one more (unpipelined) iteration from the state the pipelined run left behind
+        ctx.set_pipeline(0)
+        ctx.fine_sweep()
+        upd = ctx.parareal_correct()
+        last = host(ctx.get_slice(p.N, buf)).copy()
+        ctx.close()
+        outs.append((k, hist, traj, upd, last))
+    (k1, h1, t1, u1, l1), (k0, h0, t0, u0_, l0) = outs
+    assert k1 == k0 and (tol > 0.0 or k0 == p.N)
+    assert h1 == h0
+    assert np.array_equal(t1, t0)
+    assert u1 == u0_ and np.array_equal(l1, l0)
+    if tol == 0.0 and p.n <= 64:  # finite termination: the sequential fine solution
+        fine = oracle.Oracle(p).fine_solution(u0)
+        scale = max(float(np.max(np.abs(t))) for t in fine)
+        assert float(np.max(np.abs(t1 - fine))) / scale <= TOL
+
+
+def test_pipeline_rejects_unsupported_paths():
+    prs = prs_mod()
+    for p in (Problem(dim=2, n=512, c=1.0, N=4, s=2, G=FIE, F=FIE),
+              Problem(dim=2, n=64, c=1.0, coef=1, N=4, s=2, G=FIE, F=FIE)):
+        ctx = prs.Context(p)
+        with pytest.raises(prs.PrsError):
+            ctx.set_pipeline(2)
+        ctx.set_pipeline(0)
+        ctx.close()
+
+
 @pytest.mark.parametrize("p,bands", [
     (Problem(dim=2, n=256, c=1.0, coef=1, N=4, s=3, G=FIE, F=DR, init="modes", seed=2), 4),
     (Problem(dim=2, n=256, c=1.0, coef=1, N=5, s=2, G=FIE, F=FIE, init="modes", seed=3), 2),
