@@ -1059,6 +1059,7 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
         x.sinpi = ctx->sinpi;
         x.ta = ta;
         x.tab = CoefTab{f.tab, f.tab + XY_N, f.tab + 2 * XY_N};
+        x.offd = -f.tau * ctx->h2inv;  // as setup_const_tab forms it
         void (*kx)(XYArgs) = ctx->p.source_kind ? xy3_kernel<1> : xy3_kernel<0>;
         const size_t shm = xy3_smem_bytes();
         CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));

@@ -19,7 +19,11 @@
 //    plane load, publishes the mbarrier initialisation);
 //  * the tile uses the chunk-padded row layout (x at x + x/16, row stride 136): the x walks
 //    (rows r, r+1 x 8 chunks per half-warp) and the y walks (consecutive columns) are both
-//    bank-conflict free.
+//    bank-conflict free;
+//  * the walks read only the inverse pivots id from shared memory and form the multipliers
+//    m_i = o id_{i-1} and cc_i = o id_i (o = -tau/h^2, constant off-diagonals for kappa = 1) --
+//    the very products setup_const_tab stores, so the results are bitwise those of the full
+//    tables, with half the shared-memory traffic of the walks (the pass is bound by it).
 #pragma once
 #include "common.cuh"
 #include "lpass4.cuh"
@@ -41,6 +45,7 @@ struct XYArgs {
     const double *sinpi;
     TimeArgs ta;
     CoefTab tab;        // kappa = 1 pivots (m, id, cc), the same for x and y
+    double offd;        // the off-diagonal -tau / h^2: m_i = offd id_{i-1}, cc_i = offd id_i
 };
 
 inline size_t xy3_smem_bytes() {
@@ -107,7 +112,10 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
     {
         const int c = lane & 7;  // chunk along x
         // pivots of the chunk from the padded table: the 8 chunks of a half-warp hit 8 banks
-        const double *tm = ty + c * LCP, *ti = ty + XY_S + c * LCP, *tc = ty + 2 * XY_S + c * LCP;
+        const double *ti = ty + XY_S + c * LCP;
+        const double o = a.offd, m0 = ty[c * LCP];  // m of the chunk's first point (0 on the row's first)
+        auto tmv = [&](int i) { return i == 0 ? m0 : o * ti[i - 1]; };
+        auto tcv = [&](int i) { return (c == 7 && i == LCH - 1) ? 0.0 : o * ti[i]; };
         for (int k = 0; k < 2; ++k) {
             const int q = tid + k * XY_T;
             const int r = (q >> 5) * 4 + (lane >> 3);
@@ -118,25 +126,26 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
             double A = 1.0, B = 0.0;
 #pragma unroll
             for (int i = 0; i < LCH; ++i) {
-                B = fma(-tm[i], B, v[i]);
-                A = -tm[i] * A;
+                const double m = tmv(i);
+                B = fma(-m, B, v[i]);
+                A = -m * A;
             }
             double EA, EB;
             seg_scan_fwd(A, B, 8, c, EA, EB);
             double y = EB, Pb = 1.0, Qb = 0.0;  // y entering the chunk (y_in of the row = 0)
 #pragma unroll
             for (int i = 0; i < LCH; ++i) {
-                y = fma(-tm[i], y, v[i]);
+                y = fma(-tmv(i), y, v[i]);
                 v[i] = y;
                 Qb = fma(Pb * ti[i], y, Qb);
-                Pb *= -tc[i];
+                Pb *= -tcv(i);
             }
             double EP, EQ;
             seg_scan_bwd(Pb, Qb, 8, c, EP, EQ);
             double x = EQ;  // x leaving the chunk (x after the row's end = 0)
 #pragma unroll
             for (int i = LCH - 1; i >= 0; --i) {
-                x = fma(ti[i], v[i], -tc[i] * x);
+                x = fma(ti[i], v[i], -tcv(i) * x);
                 v[i] = x;
             }
 #pragma unroll
@@ -149,9 +158,9 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
     const int w = tid & (XY_N - 1), t0 = tid >> 7;  // column, first chunk (t0, t0 + 2)
     double v0[LCH], v1[LCH];
     Tup u0, u1;
-    auto ym = [&](int t, int i) { return ty[cpad(rg0 + t * LCH) + i]; };
     auto yi = [&](int t, int i) { return ty[XY_S + cpad(rg0 + t * LCH) + i]; };
-    auto yc = [&](int t, int i) { return ty[2 * XY_S + cpad(rg0 + t * LCH) + i]; };
+    auto ym = [&](int t, int i) { return i == 0 ? ty[cpad(rg0 + t * LCH)] : a.offd * yi(t, i - 1); };
+    auto yc = [&](int t, int i) { return (rg0 + t * LCH + i == XY_N - 1) ? 0.0 : a.offd * yi(t, i); };
     auto walk1 = [&](int t, const double (&v)[LCH]) {
         double y0 = 0.0, g = 1.0, cp = 1.0, Q = 0.0, R = 0.0;
 #pragma unroll
