@@ -10,7 +10,8 @@
 // the block solve is exactly (up to rounding)
 //     G = Q^T F  ->  (theta_a I - tau Y) v_a = g_a  (n-long tridiagonal, one per mode a)
 //     ->  U = Q V.
-// A block of one state is cut into CL row pieces of R <= 128 rows, one per CTA, each held in
+// A block of one state is cut into CL row pieces of R <= 64 rows, one per CTA (two CTAs per SM,
+// so one piece's transforms overlap another's loads, waits and walks), each held in
 // shared memory: two dense W x W transforms on the fp64 FMA pipes (register-tiled, Q streamed
 // through shared memory), and the n-long tridiagonal solves with the chunk-parallel Thomas of
 // common.cuh across the pieces.  The pieces exchange their scan totals through L2 (default: a
@@ -47,11 +48,13 @@ int prs_internal_prof_end(prs_ctx *ctx, int kind, double bytes);
 
 namespace prs {
 
-constexpr int DD_RMAX = 128;   // rows per CTA
-constexpr int DD_WMAX = 144;   // widest block (16 column groups x 9)
+constexpr int DD_RMAX = 64;    // rows per CTA (row piece)
+constexpr int DD_WMAX = 144;   // widest block (2 x 72 output columns in the GEMMs)
 constexpr int DD_WPAD = 148;   // shared row stride of a tile (>= DD_WMAX, == 4 mod 16)
-constexpr int DD_KC = 16;      // Q rows staged per k-chunk
-constexpr int DD_THREADS = 512;  // 16 warps: 32 row groups x 16 column groups in the GEMMs
+constexpr int DD_KC = 8;       // Q rows staged per k-chunk
+constexpr int DD_THREADS = 256;  // 8 warps: DD_RMAX / 16 row groups x 2 column halves (GEMM)
+constexpr int DD_NCH = DD_RMAX / 16;  // 16-row chunks of a piece (y solve)
+constexpr int DD_FTHREADS = 512;      // factorisation kernel
 
 // ------------------------------------------------------------- partition of unity --
 // rho_0 at a 1-based position xpos (integer = node, half-integer = face), index-space
@@ -110,7 +113,7 @@ struct DDBlock {
     double *Q = nullptr, *QT = nullptr, *theta = nullptr, *idy = nullptr;  // per tau slot
 };
 
-__global__ void __launch_bounds__(DD_THREADS) dd_factor_kernel(int n, int i0, int W, const double *rhon,
+__global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, int W, const double *rhon,
                                                                const double *rhof, double tau, double h2inv,
                                                                double c, double *Z, double *Q, double *QT,
                                                                double *theta, double *idy, int sweeps) {
@@ -294,14 +297,14 @@ __device__ __forceinline__ void dmma_f64(double &c0, double &c1, double a, doubl
         : "d"(a), "d"(b));
 }
 __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
-    // fp64 tensor-core MMA (m8n8k4): warp w owns rows 16 (w & 7) .. +15 and columns
-    // 72 (w >> 3) .. +71 of the output, i.e. 2 x 9 tiles of 8 x 8, accumulators in registers.
+    // fp64 tensor-core MMA (m8n8k4): warp w owns rows 16 (w % NCH) .. +15 and columns
+    // 72 (w / NCH) .. +71 of the output, i.e. 2 x 9 tiles of 8 x 8, accumulators in registers.
     // Per 4-wide k step: 2 A fragments (A[r][k], r = lane / 4, k = lane % 4) from the tile and 9
     // B fragments (B[k][c], k = lane % 4, c = lane / 4) from the staged chunk, all bank-conflict
     // free with the 148-double row stride; 18 MMAs of 256 FMAs each.
-    static_assert(DD_THREADS == 512 && DD_RMAX == 128 && DD_WMAX == 144 && DD_KC % 4 == 0, "dmma tiling");
+    static_assert(DD_THREADS / 32 == 2 * DD_NCH && DD_WMAX == 144 && DD_KC % 4 == 0, "dmma tiling");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rb = 16 * (warp & 7), cb = 72 * (warp >> 3);
+    const int rb = 16 * (warp % DD_NCH), cb = 72 * (warp / DD_NCH);
     const int fr = lane >> 2, fk = lane & 3;
     double acc[2][9][2];
 #pragma unroll
@@ -472,7 +475,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
 
     // ---- (theta_a I - tau Y) v_a = g_a along y: warp = chunk t (of 16 rows) x mode half,
     // lanes = modes: half 0 walks mode rounds 0..2 (modes 0..95), half 1 rounds 3..4 ----
-    const int t = (tid >> 5) & 7, lane = tid & 31, mh = tid >> 8;
+    const int t = (tid >> 5) % DD_NCH, lane = tid & 31, mh = (tid >> 5) / DD_NCH;
     const int e0 = t * LCH;
     const int cnt = max(0, min(LCH, nrow - e0));
     const double ms = -a.tau * a.h2inv;  // off-diagonal of theta I - tau Y
@@ -766,7 +769,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
 // the same block, which the earliest unfinished block always has CTAs free to take, so the
 // in-order hand-out cannot deadlock.  No SM idles for want of a whole free cluster.
 template <int DR, int SRC, int GX>
-__global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
+__global__ void __launch_bounds__(DD_THREADS, 2) dd_stage_kernel(DDStageArgs a) {
     extern __shared__ double sh[];
     if (GX) {
         __shared__ int s_task;
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(DD_THREADS) dd_stage_kernel(DDStageArgs a) {
 
 inline size_t dd_stage_smem_bytes() {
     // tile + two staged M chunks (the y-solve chunk maps alias them) + cluster totals
-    static_assert(2 * DD_KC * DD_WPAD * sizeof(double) >= 8 * DD_WMAX * sizeof(double2), "sc alias");
+    static_assert(2 * DD_KC * DD_WPAD * sizeof(double) >= DD_NCH * DD_WMAX * sizeof(double2), "sc alias");
     return sizeof(double) * ((size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD + 2 * DD_KC * DD_WPAD) +
            sizeof(double2) * (2 * DD_WMAX);
 }
@@ -841,7 +844,7 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
         err = "DD GPU path needs at least 2 strips and an overlap of at least 2 cells";
         return PRS_EUNSUPPORTED;
     }
-    if ((d.n + DD_RMAX - 1) / DD_RMAX > 8) {
+    if ((d.n + DD_RMAX - 1) / DD_RMAX > 16) {
         err = "DD GPU path supports n <= 1024";
         return PRS_EUNSUPPORTED;
     }
@@ -909,7 +912,7 @@ inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
                 return PRS_ECUDA;
             }
             d.store[slot].insert(d.store[slot].end(), {Q, QT, th, idy});
-            dd_factor_kernel<<<1, DD_THREADS, fsm, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
+            dd_factor_kernel<<<1, DD_FTHREADS, fsm, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
                                                          d.rhof + col * (d.n + 1), tau, d.h2inv, d.c, d.Z, Q, QT,
                                                          th, idy, 14);
             hQ[k] = Q;
@@ -1020,10 +1023,18 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
             return PRS_ECUDA;
         }
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)(d.gx ? std::min<long long>(ntasks, d.num_sms) : ntasks));
+        int per_sm = 1;  // persistent grid: every co-resident CTA slot
+        if (d.gx && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DD_THREADS, shm) != cudaSuccess)
+            per_sm = 1;
+        per_sm = std::max(per_sm, 1);
+        cfg.gridDim = dim3((unsigned)(d.gx ? std::min<long long>(ntasks, (long long)per_sm * d.num_sms) : ntasks));
         cfg.blockDim = dim3(DD_THREADS);
         cfg.dynamicSmemBytes = shm;
         cfg.stream = st;
+        if (!d.gx && CL > 8) {
+            err = "DD cluster exchange (PRS_DDCL=1): at most 8 row pieces per block";
+            return PRS_EUNSUPPORTED;
+        }
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = CL;
