@@ -2014,7 +2014,7 @@ int prs_set_pipeline(prs_ctx *ctx, int blocks) {
 
 int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
     if (!ctx || kmax < 0) return PRS_EINVAL;
-    if (ctx->pipe) {
+    if (ctx->pipe && !ctx->gpar) {  // (space-parallel G takes the unpipelined chain)
         if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
         return pipe_iterate(ctx, kmax < ctx->p.N ? kmax : ctx->p.N, tol, k_out, hist);
     }
