@@ -341,6 +341,7 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
             const double a0 = ta0[k0 + kq], a1 = ta1[k0 + kq];
 #pragma unroll
             for (int j = 0; j < 9; ++j) {
+                if (j == 8 && cb + 64 >= W) break;  // (warp-uniform) a tile of padding columns only
                 const double bv = tb[kq * DD_WPAD + 8 * j];
                 dmma_f64(acc[0][j][0], acc[0][j][1], a0, bv);
                 dmma_f64(acc[1][j][0], acc[1][j][1], a1, bv);
