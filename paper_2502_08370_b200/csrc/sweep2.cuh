@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
         mbar_fence_init();
         mbar_arrive_expect(&mbe, ebytes);  // step 0's halo rows
     }
-    if (HALO) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    if (HALO) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 
     for (int e = tid; e < N; e += SW_T) {
         tb[cpad(e)] = __ldg(a.tab.m + e);

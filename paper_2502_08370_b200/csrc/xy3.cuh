@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
         mbar_fence_init();
         mbar_arrive_expect(&mbx, XY_N * sizeof(double2));
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     const long long plane = blockIdx.x / 2;
     const long long b = plane / XY_N;
     const int z = (int)(plane - b * XY_N);
