@@ -44,7 +44,9 @@ typedef struct prs_problem {
     int dim;          /* 2 or 3                                                          */
     int n;            /* interior nodes per axis (>= 1)                                  */
     double c;         /* reaction coefficient, L u = div(kappa grad u) - c u */
-    int coef_kind;    /* 0: kappa = 1;  1: kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y) (2-D) */
+    int coef_kind;    /* 0: kappa = 1;  1: kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y) (2-D);
+                         2: the full tensor of PAPER.md:523-528 (NEXT-3) -- PRS_EUNSUPPORTED
+                            on the GPU path for now (the CPU oracle implements it) */
     int split;        /* 0: dimensional, M = dim;  1: domain decomposition, M = 2 (2-D)  */
     int dd_strips;    /* DD: number of vertical strips 2q (n % dd_strips == 0)           */
     int dd_overlap;   /* DD: overlap width in cells (even, < n/dd_strips)                */

@@ -108,7 +108,7 @@ class Oracle:
         return self.L.orc_rho(self.p, j, xpos)
 
     def row(self, term, i, l, m=1):
-        out = np.zeros(7)
+        out = np.zeros(11)
         self.L.orc_row(self.p, term, i, l, m, _dp(out))
         return out
 

@@ -54,6 +54,69 @@ static double kappa_at(const orc_problem *p, double x, double y) {
     return 1.0;
 }
 
+double orc_rho(const orc_problem *p, int j, double xpos); /* partition of unity, below */
+
+/* coef == 2: the full diffusion tensor of PAPER.md:523-528 (section 5.2),
+ * d11 = d22 = 1 / (2 + cos(3 pi x) cos(2 pi y)), d12 = 1/4. */
+static double dfull_diag(double x, double y) { return 1.0 / (2.0 + cos(3.0 * ORC_PI * x) * cos(2.0 * ORC_PI * y)); }
+static double dfull_offd(double x, double y) { (void)x; (void)y; return 0.25; }
+
+/* Row of the full-tensor operator (coef == 2, 2-D) into the 3 x 3 stencil cf[di+1][dl+1]:
+ *   L_j u = div(rho_j D grad u) - rho_j c u   (unsplit: rho = 1)
+ * discretised conservatively: flux differences over the four faces of the node's
+ * cell, (F^x_{i+1/2} - F^x_{i-1/2}) / h + (F^y_{l+1/2} - F^y_{l-1/2}) / h, with
+ *   F^x_{i+1/2,l} = rho(i+1/2) [ d11 (u_{i+1,l} - u_{i,l}) / h + avg over the corners
+ *                   (i+1/2, l +- 1/2) of d12 (u_y)_corner ]
+ *   F^y_{i,l+1/2} = rho(i) d22 (u_{i,l+1} - u_{i,l}) / h + avg over the corners
+ *                   (i +- 1/2, l+1/2) of rho(corner x) d12 (u_x)_corner
+ * where a corner derivative is the mean of the two differences across the corner's cell
+ * side, e.g. (u_x)_(i+1/2,l+1/2) = [(u_{i+1,l} - u_{i,l}) + (u_{i+1,l+1} - u_{i,l+1})] / 2h.
+ * Readings (R21, R22): the paper does not give its mixed-derivative stencil
+ * (SPEC.md:92, 103); this is the standard 9-point cross scheme (for rho = 1 the mixed part is
+ * d12 (u_{i+1,l+1} - u_{i+1,l-1} - u_{i-1,l+1} + u_{i-1,l-1}) / (2 h^2)), with d12 taken at the
+ * corners ("the four diagonal neighbours' midpoints").  The DD weight of a mixed
+ * flux piece is rho_j at its corner's x (rho depends on x only): at a block's edge columns the
+ * corner weights vanish with the face weight, so (I - tau A_j) stays block diagonal
+ * and sum_j A_j = A by linearity. */
+static void row_full(const orc_problem *p, int term, int i, int l, double cf[3][3]) {
+    double h = grid_h(p), h2 = h * h;
+    double x = i * h, y = l * h;
+    double rxm = 1.0, rxp = 1.0, rn = 1.0;
+    if (term >= 0) {
+        rxm = orc_rho(p, term, (double)i - 0.5);
+        rxp = orc_rho(p, term, (double)i + 0.5);
+        rn = orc_rho(p, term, (double)i);
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) cf[a][b] = 0.0;
+#define ADD(di, dl, v) (cf[(di) + 1][(dl) + 1] += (v))
+    /* diffusion: x faces (d11 at (x_{i -+ 1/2}, y_l)), y faces (d22 at (x_i, y_{l -+ 1/2})) */
+    double axp = rxp * dfull_diag(((double)i + 0.5) * h, y) / h2;
+    double axm = rxm * dfull_diag(((double)i - 0.5) * h, y) / h2;
+    double ayp = rn * dfull_diag(x, ((double)l + 0.5) * h) / h2;
+    double aym = rn * dfull_diag(x, ((double)l - 0.5) * h) / h2;
+    ADD(1, 0, axp); ADD(0, 0, -axp);
+    ADD(-1, 0, axm); ADD(0, 0, -axm);
+    ADD(0, 1, ayp); ADD(0, 0, -ayp);
+    ADD(0, -1, aym); ADD(0, 0, -aym);
+    /* mixed: corner (sx/2, sy/2) relative to the node, sx, sy in {-1, +1} */
+    for (int sx = -1; sx <= 1; sx += 2)
+        for (int sy = -1; sy <= 1; sy += 2) {
+            double xc = ((double)i + 0.5 * sx) * h, yc = ((double)l + 0.5 * sy) * h;
+            double rc = (sx > 0) ? rxp : rxm;       /* rho at the corner's x */
+            double g = rc * dfull_offd(xc, yc) / (4.0 * h2); /* 1/2 (avg) x 1/(2h) x 1/h */
+            /* x-face term: sign sx (outer difference), d12 (u_y)_corner, u_y across the corner
+             * in direction sy: nodes (0 or sx, sy) minus (0 or sx, 0) times sy */
+            double gx = sx * sy * g;
+            ADD(0, sy, gx); ADD(0, 0, -gx); ADD(sx, sy, gx); ADD(sx, 0, -gx);
+            /* y-face term: sign sy, d12 (u_x)_corner, u_x across the corner in direction sx */
+            double gy = sy * sx * g;
+            ADD(sx, 0, gy); ADD(0, 0, -gy); ADD(sx, sy, gy); ADD(0, sy, -gy);
+        }
+#undef ADD
+    cf[1][1] -= rn * p->c; /* reaction, rho_j at the node */
+}
+
 /* ------------------------------------------------------ partition of unity -- */
 /* Strip geometry in index space (reading R6): S = dd_strips strips of
  * w = n/S nodes; interface m (m = 1..S-1) at 1-based position w m + 1/2; the ramp of
@@ -105,18 +168,35 @@ double orc_rho(const orc_problem *p, int j, double xpos) {
 
 /* ---------------------------------------------------------- operator rows -- */
 /* Row of a (sub)operator at node (i, l, m): coefficients of
- *   out[0] centre, out[1] (-x), out[2] (+x), out[3] (-y), out[4] (+y), out[5] (-z), out[6] (+z).
+ *   out[0] centre, out[1] (-x), out[2] (+x), out[3] (-y), out[4] (+y), out[5] (-z), out[6] (+z),
+ *   and for the full tensor (coef == 2) the corners out[7] (-x,-y), out[8] (+x,-y),
+ *   out[9] (-x,+y), out[10] (+x,+y).
  * term = -1 : the unsplit A;
  * split == 0: term d = dimension d, L_d u = (kappa u_{x_d})_{x_d} - (c/M) u;
  * split == 1: term j = colour j, L_j u = div(rho_j kappa grad u) - rho_j c u,
  *             x-faces weighted by rho_j at the face, y-faces and reaction by rho_j at the node
  *             (SPEC.md:147).  Neighbours outside the domain are Dirichlet zero: their
  *             coefficient is still present in the centre but the off-diagonal is dropped. */
-void orc_row(const orc_problem *p, int term, int i, int l, int m, double out[7]) {
+void orc_row(const orc_problem *p, int term, int i, int l, int m, double out[11]) {
     double h = grid_h(p), h2 = h * h;
     int n = p->n, M = p->dim;
     double x = i * h, y = l * h;
-    for (int k = 0; k < 7; ++k) out[k] = 0.0;
+    for (int k = 0; k < 11; ++k) out[k] = 0.0;
+    if (p->coef == 2) { /* full tensor (2-D; dimensional splitting does not apply) */
+        double cf[3][3];
+        row_full(p, term, i, l, cf);
+        out[0] = cf[1][1];
+        if (i > 1) out[1] = cf[0][1];
+        if (i < n) out[2] = cf[2][1];
+        if (l > 1) out[3] = cf[1][0];
+        if (l < n) out[4] = cf[1][2];
+        if (i > 1 && l > 1) out[7] = cf[0][0];
+        if (i < n && l > 1) out[8] = cf[2][0];
+        if (i > 1 && l < n) out[9] = cf[0][2];
+        if (i < n && l < n) out[10] = cf[2][2];
+        (void)m; (void)x; (void)y; (void)h2; (void)M;
+        return;
+    }
     double cen = 0.0;
     /* face coefficients kappa at midpoints; a face coordinate is formed from its
      * half-integer index, ((double)i + 0.5) h, so both neighbours see the same value */
@@ -161,7 +241,7 @@ void orc_row(const orc_problem *p, int term, int i, int l, int m, double out[7])
 void orc_apply(const orc_problem *p, int term, const double *u, double *out) {
     int n = p->n, nz = (p->dim == 3) ? n : 1;
     long sy = n, sz = (long)n * n;
-    double r[7];
+    double r[11];
     for (int m = 1; m <= nz; ++m)
         for (int l = 1; l <= n; ++l)
             for (int i = 1; i <= n; ++i) {
@@ -176,6 +256,12 @@ void orc_apply(const orc_problem *p, int term, const double *u, double *out) {
                     if (m > 1) v += r[5] * u[P - sz];
                     if (m < n) v += r[6] * u[P + sz];
                 }
+                if (p->coef == 2) {
+                    if (i > 1 && l > 1) v += r[7] * u[P - sy - 1];
+                    if (i < n && l > 1) v += r[8] * u[P - sy + 1];
+                    if (i > 1 && l < n) v += r[9] * u[P + sy - 1];
+                    if (i < n && l < n) v += r[10] * u[P + sy + 1];
+                }
                 out[P] = v;
             }
 }
@@ -184,7 +270,7 @@ void orc_apply(const orc_problem *p, int term, const double *u, double *out) {
 void orc_dense(const orc_problem *p, int term, double *Mat) {
     int n = p->n, nz = (p->dim == 3) ? n : 1;
     long N = npoints(p), sy = n, sz = (long)n * n;
-    double r[7];
+    double r[11];
     memset(Mat, 0, sizeof(double) * N * N);
     for (int m = 1; m <= nz; ++m)
         for (int l = 1; l <= n; ++l)
@@ -199,6 +285,12 @@ void orc_dense(const orc_problem *p, int term, double *Mat) {
                 if (p->dim == 3) {
                     if (m > 1) Mat[P * N + P - sz] = r[5];
                     if (m < n) Mat[P * N + P + sz] = r[6];
+                }
+                if (p->coef == 2) {
+                    if (i > 1 && l > 1) Mat[P * N + P - sy - 1] = r[7];
+                    if (i < n && l > 1) Mat[P * N + P - sy + 1] = r[8];
+                    if (i > 1 && l < n) Mat[P * N + P + sy - 1] = r[9];
+                    if (i < n && l < n) Mat[P * N + P + sy + 1] = r[10];
                 }
             }
 }
@@ -251,7 +343,7 @@ static void solve_dim(const orc_problem *p, int d, double tau, const double *r, 
     double *a = malloc(sizeof(double) * n), *b = malloc(sizeof(double) * n),
            *c = malloc(sizeof(double) * n), *x = malloc(sizeof(double) * n),
            *w = malloc(sizeof(double) * n);
-    double row[7];
+    double row[11];
     memcpy(v, r, sizeof(double) * N);
     for (int m = 1; m <= nz; ++m)
         for (int l = 1; l <= n; ++l)
@@ -287,7 +379,7 @@ static void solve_dd(const orc_problem *p, int j, double tau, const double *r, d
     long N = npoints(p);
     memcpy(v, r, sizeof(double) * N);
     int i = 1;
-    double row[7];
+    double row[11];
     while (i <= n) {
         if (!(orc_rho(p, j, (double)i) > 0.0)) { ++i; continue; }
         int i0 = i;
@@ -295,7 +387,7 @@ static void solve_dd(const orc_problem *p, int j, double tau, const double *r, d
         int i1 = i - 1;
         int W = i1 - i0 + 1;
         long Nb = (long)W * n;
-        int bw = W;
+        int bw = (p->coef == 2) ? W + 1 : W; /* 9-point rows reach q -+ (W +- 1) */
         long ld = 2L * bw + 1;
         double *Ab = calloc((size_t)(Nb * ld), sizeof(double));
         double *bb = malloc(sizeof(double) * Nb);
@@ -309,6 +401,12 @@ static void solve_dd(const orc_problem *p, int j, double tau, const double *r, d
                 if (ii < i1) Ab[q * ld + bw + 1] = -tau * row[2];
                 if (l > 1) Ab[q * ld + bw - W] = -tau * row[3];
                 if (l < n) Ab[q * ld + bw + W] = -tau * row[4];
+                if (p->coef == 2) {
+                    if (ii > i0 && l > 1) Ab[q * ld + bw - W - 1] = -tau * row[7];
+                    if (ii < i1 && l > 1) Ab[q * ld + bw - W + 1] = -tau * row[8];
+                    if (ii > i0 && l < n) Ab[q * ld + bw + W - 1] = -tau * row[9];
+                    if (ii < i1 && l < n) Ab[q * ld + bw + W + 1] = -tau * row[10];
+                }
                 bb[q] = r[node_index(p, ii, l, 1)];
             }
         /* forward elimination */

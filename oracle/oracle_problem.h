@@ -7,7 +7,9 @@ typedef struct {
     int dim;        /* 2 or 3 spatial dimensions (unit square / cube)                 */
     int n;          /* interior nodes per axis, h = 1/(n+1)                           */
     double c;       /* reaction coefficient c > 0                        */
-    int coef;       /* 0: kappa = 1;  1: kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y)       */
+    int coef;       /* 0: kappa = 1;  1: kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y);
+                       2: full tensor d11 = d22 = 1/(2 + cos 3pi x cos 2pi y), d12 = 1/4
+                          (2-D, DD splitting only)                       */
     int split;      /* 0: dimensional; 1: domain decomposition (2-D)  */
     int dd_strips;  /* DD: total number of vertical strips (2q)           */
     int dd_overlap; /* DD: overlap width beta in cells                                 */

@@ -1124,7 +1124,11 @@ static int validate(const prs_problem *p, std::string &err) {
         err = "schemes must be PRS_FIE or PRS_DR";
         return PRS_EINVAL;
     }
-    if (p->coef_kind != 0 && p->coef_kind != 1) { err = "coef_kind must be 0 or 1"; return PRS_EINVAL; }
+    if (p->coef_kind == 2) {
+        err = "full diffusion tensor (coef_kind 2, PAPER.md:520-546, NEXT-3): CPU oracle only so far";
+        return PRS_EUNSUPPORTED;
+    }
+    if (p->coef_kind != 0 && p->coef_kind != 1) { err = "coef_kind must be 0, 1 or 2"; return PRS_EINVAL; }
     if (p->source_kind != 0 && p->source_kind != 1) { err = "source_kind must be 0 or 1"; return PRS_EINVAL; }
     if (p->split != 0 && p->split != 1) { err = "split must be 0 or 1"; return PRS_EINVAL; }
     if (p->split == 1) {

@@ -26,7 +26,8 @@ class Problem:
     dim: int = 2
     n: int = 32
     c: float = 1.0
-    coef: int = 0          # 0 kappa = 1, 1 kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y)
+    coef: int = 0          # 0 kappa = 1, 1 kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y),
+                           # 2 full tensor of section 5.2 (DD only; oracle only, NEXT-3)
     split: int = 0         # 0 dimensional, 1 domain decomposition
     dd_strips: int = 8
     dd_overlap: int = 8

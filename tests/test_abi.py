@@ -67,7 +67,8 @@ def test_create_rejects_invalid_configs_before_touching_the_gpu():
         with pytest.raises(prs.PrsError) as ei:
             prs.Context(p)
         assert ei.value.code == prs.PRS_EINVAL
-    for p in [synth.Problem(dim=3, G=synth.DR), synth.Problem(dim=3, coef=1)]:
+    for p in [synth.Problem(dim=3, G=synth.DR), synth.Problem(dim=3, coef=1),
+              synth.Problem(coef=2, split=1, n=32, dd_strips=4, dd_overlap=4)]:
         with pytest.raises(prs.PrsError) as ei:
             prs.Context(p)
         assert ei.value.code == prs.PRS_EUNSUPPORTED

@@ -488,3 +488,106 @@ def test_c1_paper_pairing_fie_dr_contracts_per_mode():
         for k in range(1, 5):
             ek = max(abs(x - y) for x, y in zip(trs[k][1:], fine[1:]))
             assert float(ek) <= K ** k * float(e0) * (1 + 1e-9) + 1e-30, (j, l, k, float(ek), K)
+
+
+# --------------------------- NEXT-3: full diffusion tensor (section 5.2)
+# d11 = d22 = 1 / (2 + cos(3 pi x) cos(2 pi y)), d12 = 1/4; DD splitting only (mixed
+# derivatives).  DESIGN.md R21 (9-point cross stencil, d12 at the cell corners)
+# and R22 (DD weight of a mixed flux piece = rho_j at its corner's x).
+
+def _lu_exact_full_tensor(x, y, c):
+    """L u = div(D grad u) - c u for u = sin(2 pi x) sin(2 pi y) and the section-5.2 tensor,
+    differentiated by hand: (d u_x)_x + (d u_y)_y + 2 d12 u_xy - c u with d = 1/g,
+    g = 2 + cos(3 pi x) cos(2 pi y) (constant d12)."""
+    pi = np.pi
+    u = np.sin(2 * pi * x) * np.sin(2 * pi * y)
+    ux = 2 * pi * np.cos(2 * pi * x) * np.sin(2 * pi * y)
+    uy = 2 * pi * np.sin(2 * pi * x) * np.cos(2 * pi * y)
+    uxx = -4 * pi ** 2 * u
+    uyy = -4 * pi ** 2 * u
+    uxy = 4 * pi ** 2 * np.cos(2 * pi * x) * np.cos(2 * pi * y)
+    g = 2 + np.cos(3 * pi * x) * np.cos(2 * pi * y)
+    gx = -3 * pi * np.sin(3 * pi * x) * np.cos(2 * pi * y)
+    gy = -2 * pi * np.cos(3 * pi * x) * np.sin(2 * pi * y)
+    d, dx, dy = 1 / g, -gx / g ** 2, -gy / g ** 2
+    return u, dx * ux + d * uxx + dy * uy + d * uyy + 2 * 0.25 * uxy - c * u
+
+
+def test_full_tensor_operator_is_second_order():
+    """the discrete full-tensor operator on the interpolant of sin(2 pi x)
+    sin(2 pi y) matches L u pointwise to O(h^2), slope ~ 2 over h = 1/32, 1/64, 1/128."""
+    errs, hs = [], []
+    for n in (31, 63, 127):
+        p = Problem(dim=2, n=n, c=1.0, coef=2, split=1, dd_strips=2, dd_overlap=2)
+        o = oracle.Oracle(p)
+        h = 1.0 / (n + 1)
+        xs = h * np.arange(1, n + 1)
+        X, Y = np.meshgrid(xs, xs)
+        u, lu = _lu_exact_full_tensor(X, Y, 1.0)
+        errs.append(np.max(np.abs(o.apply(-1, u) - lu)))
+        hs.append(h)
+    slope = np.polyfit(np.log(hs), np.log(errs), 1)[0]
+    assert 1.8 <= slope <= 2.2, (errs, slope)
+
+
+def test_full_tensor_mixed_stencil_is_the_cross_difference():
+    """For rho = 1 away from the boundary the row is the conservative 5-point part plus
+    d12 (u_{++} - u_{+-} - u_{-+} + u_{--}) / (2 h^2): corners +-d12/(2h^2), and the mixed
+    contributions cancel on the centre and the four edge neighbours (row sum = -c for a
+    constant field's interior row)."""
+    n = 15
+    p = Problem(dim=2, n=n, c=0.7, coef=2, split=1, dd_strips=2, dd_overlap=2)
+    o = oracle.Oracle(p)
+    h = 1.0 / (n + 1)
+    i, l = 7, 9
+    r = o.row(-1, i, l)
+    g = 0.25 / (2 * h * h)
+    assert r[10] == pytest.approx(g, rel=1e-14) and r[7] == pytest.approx(g, rel=1e-14)
+    assert r[8] == pytest.approx(-g, rel=1e-14) and r[9] == pytest.approx(-g, rel=1e-14)
+    d = lambda x, y: 1.0 / (2 + np.cos(3 * np.pi * x) * np.cos(2 * np.pi * y))
+    x, y = i * h, l * h
+    assert r[1] == pytest.approx(d(x - h / 2, y) / h ** 2, rel=1e-13)
+    assert r[2] == pytest.approx(d(x + h / 2, y) / h ** 2, rel=1e-13)
+    assert r[3] == pytest.approx(d(x, y - h / 2) / h ** 2, rel=1e-13)
+    assert r[4] == pytest.approx(d(x, y + h / 2) / h ** 2, rel=1e-13)
+    assert sum(r) == pytest.approx(-0.7, abs=1e-9 / h ** 2)
+
+
+FULL_DD = [
+    Problem(dim=2, n=32, c=1.0, coef=2, split=1, dd_strips=4, dd_overlap=4, dd_ramp=0),
+    Problem(dim=2, n=32, c=1.0, coef=2, split=1, dd_strips=4, dd_overlap=4, dd_ramp=1),
+    Problem(dim=2, n=24, c=2.0, coef=2, split=1, dd_strips=8, dd_overlap=2, dd_ramp=0),
+]
+
+
+@pytest.mark.parametrize("p", FULL_DD, ids=lambda p: f"n{p.n}_S{p.dd_strips}_b{p.dd_overlap}_r{p.dd_ramp}")
+def test_full_tensor_dd_split(p):
+    """The unsplit operator is symmetric and negative definite; sum_j A_j = A to
+    1e-13; each (I - tau A_j) is block diagonal with identity rows outside the
+    support of rho_j -- the corner weights of R22 vanish at the
+    block edges -- and the oracle's band elimination equals LAPACK's dense solve."""
+    o = oracle.Oracle(p)
+    A = o.dense(-1)
+    assert np.max(np.abs(A - A.T)) <= 1e-13 * np.max(np.abs(A))
+    assert np.max(np.linalg.eigvalsh(0.5 * (A + A.T))) < 0.0
+    terms = [o.dense(j) for j in range(2)]
+    assert np.max(np.abs(terms[0] + terms[1] - A)) <= 1e-13 * np.max(np.abs(A))
+    n = p.n
+    col = np.tile(np.arange(1, n + 1), n)  # x index (1-based) of every unknown, x-fastest
+    rng = np.random.default_rng(5)
+    for j in range(2):
+        sup = np.array([o.rho(j, float(i)) > 0.0 for i in range(1, n + 1)])
+        insup = sup[col - 1]
+        # block id per column: connected runs of the support
+        bid = np.cumsum(np.concatenate([[1], (sup[1:] & ~sup[:-1]).astype(int)])) * sup
+        B = np.eye(A.shape[0]) - 0.05 * terms[j]
+        # identity rows outside the support
+        assert np.array_equal(B[~insup], np.eye(A.shape[0])[~insup])
+        # no coupling between different blocks or from a block to outside nodes
+        bcol = bid[col - 1]
+        for q in np.flatnonzero(insup):
+            nz = np.flatnonzero(B[q])
+            assert np.all(bcol[nz] == bcol[q]), (j, q)
+        r = rng.standard_normal(A.shape[0])
+        v = o.solve(j, 0.05, r).reshape(-1)
+        assert np.max(np.abs(v - np.linalg.solve(B, r))) <= 1e-12 * np.max(np.abs(r))
