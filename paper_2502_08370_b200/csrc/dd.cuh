@@ -291,6 +291,14 @@ __device__ __forceinline__ void dd_stage_mchunk(const double *M, int W, int k0, 
         }
     }
 }
+// one contiguous global -> shared copy on the async (TMA) engine, completing on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(mb))
+                 : "memory");
+}
+
 __device__ __forceinline__ void dmma_f64(double &c0, double &c1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(c0), "+d"(c1)
@@ -323,17 +331,47 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
             last[(kl + r) * DD_WPAD + (e - r * DD_WMAX)] = 0.0;
         }
     }
+    // chunks of M: even W -> one bulk copy per row (W * 8 bytes, 16-byte aligned) by thread 0,
+    // completing on the buffer's mbarrier; odd W -> 8-byte cp.async by all threads
+    __shared__ __align__(8) unsigned long long mbq[2];
+    const bool bulk = (W & 1) == 0;
+    if (bulk && tid == 0) {
+        mbar_init(&mbq[0], 1);
+        mbar_init(&mbq[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
-    dd_stage_mchunk(M, W, 0, Ms);
-    cp_async_commit();
+    auto stage = [&](int kb) {
+        double *dst = Ms + (kb & 1) * DD_KC * DD_WPAD;
+        if (bulk) {
+            if (tid == 0) {
+                const int k0 = kb * DD_KC, kc = min(DD_KC, W - k0);
+                // the buffer was last touched by generic loads / stores (previous chunk, y-solve
+                // scratch): order them before the async-proxy writes
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                mbar_arrive_expect(&mbq[kb & 1], (unsigned)(kc * W * sizeof(double)));
+                for (int r = 0; r < kc; ++r)
+                    bulk_g2s(dst + r * DD_WPAD, M + (long long)(k0 + r) * W, (unsigned)(W * sizeof(double)),
+                             &mbq[kb & 1]);
+            }
+        } else {
+            dd_stage_mchunk(M, W, kb * DD_KC, dst);
+        }
+        cp_async_commit();
+    };
+    stage(0);
     const double *ta0 = T + cpad(rb + fr) * DD_WPAD + fk;
     const double *ta1 = T + cpad(rb + 8 + fr) * DD_WPAD + fk;
     for (int kb = 0; kb < nk; ++kb) {
         double *cur = Ms + (kb & 1) * DD_KC * DD_WPAD;
-        if (kb + 1 < nk) dd_stage_mchunk(M, W, (kb + 1) * DD_KC, Ms + ((kb + 1) & 1) * DD_KC * DD_WPAD);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+        if (kb + 1 < nk) stage(kb + 1);
+        else cp_async_commit();
+        if (bulk) {
+            mbar_wait(&mbq[kb & 1], (unsigned)((kb >> 1) & 1));  // this chunk's bytes have landed
+        } else {
+            cp_async_wait<1>();
+            __syncthreads();
+        }
         const int k0 = kb * DD_KC;
         const double *tb = cur + fk * DD_WPAD + cb + fr;
 #pragma unroll
