@@ -4,11 +4,12 @@
 // Every slice of a fine sweep uses the same stage matrices, so the per-point pivots of a tile
 // (and the face / node sines) are the same for all of them.  A CTA here owns one tile
 // position and a group of S consecutive slices: it loads the tile's coefficients into
-// registers once, then streams the slices' state tiles through a 3-slot shared-memory ring
-// with cp.async (two tiles in flight while one is computed).  DRAM traffic per point drops
-// from state + pivots to state + pivots / S, and the copies in flight no longer depend on
-// the per-thread register loads of the compute (lp5 with slice-fastest order became
-// latency-bound exactly there: profiles/r01_fused_notes.md).  The arithmetic per tile is
+// registers once, then streams the slices' state tiles through a shared-memory ring with
+// cp.async (3 slots at two CTAs per SM for the tuple kernel; 4 slots, also carrying each
+// tile's boundary values, for the finish at one CTA per SM with the whole register file).
+// DRAM traffic per point drops from state + pivots to state + pivots / S, and the copies in
+// flight no longer depend on the per-thread register loads of the compute (lp5 with
+// slice-fastest order became latency-bound exactly there: profiles/r01_fused_notes.md).  The arithmetic per tile is
 // lpass5's (walk, 4-chunk tuple composition, exact forward / backward recurrences, fused
 // parareal epilogue).
 #pragma once

@@ -6,12 +6,14 @@
 // of CL CTAs holds one slice for all s steps: each CTA keeps 32 rows in shared memory, so the
 // state is read once at the start and Delta_n = F^s(U) - G(U) written once at the end.
 // Per step (PAPER.md:153-157 FIE, 167-171 DR in the M = 2 form of DESIGN.md R1):
-//  * x stage: rows are CTA-local; r_1 = U (+ tau A_y U for DR, rows j +- 1 of the neighbour
-//    CTAs read through distributed shared memory) (+ tau F); chunk-parallel Thomas with
-//    segmented warp scans over the CH = n/16 chunks of a row; r_2 = V_1 (- w) in place;
+//  * x stage: rows are CTA-local; r_1 = U (+ tau A_y U for DR: rows j +- 1 of the neighbour
+//    CTAs arrive as st.async messages into a parity slot, completing on this CTA's mbarrier)
+//    (+ tau F); chunk-parallel Thomas with segmented warp scans over the CH = n/16 chunks of a
+//    row; r_2 = V_1 (- w) in place;
 //  * y stage: columns cross the cluster: each thread walks 16-row chunks (lpass4.cuh 5-tuples),
-//    the CTA totals per column are exchanged through distributed shared memory (every CTA
-//    composes the totals of the CTAs before and after it), then the exact recurrences.
+//    the CTA totals per column (double-buffered by step parity) are read through distributed
+//    shared memory after the step's one cluster barrier (every CTA composes the totals of the
+//    CTAs before and after it), then the exact recurrences.
 // Pivot tables (kappa = 1: the same for x and y) sit chunk-padded in shared memory.
 // CHAIN = 1 reuses the step for the coarse chain of the parareal correction:
 // one cluster advances U_i -> G(U_i) slice after slice with the state on chip, applying the
