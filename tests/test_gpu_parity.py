@@ -284,6 +284,46 @@ def _parareal_vs_oracle(p):
     assert float(np.max(np.abs(gtrajs[K] - fine))) / scale <= TOL
 
 
+DEGENERATE_CASES = [
+    Problem(dim=2, n=1, c=1.0, N=3, s=2, G=FIE, F=DR),                    # a single grid node
+    Problem(dim=3, n=1, c=1.0, source=1, N=3, s=2, G=FIE, F=FIE),
+    Problem(dim=2, n=16, c=0.0, N=1, s=4, G=FIE, F=FIE),                  # one slice, no reaction
+    Problem(dim=2, n=16, c=1.0, source=1, N=4, s=1, G=FIE, F=FIE),        # s = 1, F = G: Delta = 0
+    Problem(dim=2, n=16, c=0.0, coef=1, N=4, s=1, G=DR, F=DR, init="modes", seed=2),
+    Problem(dim=2, n=8, c=1.0, split=1, dd_strips=2, dd_overlap=2, source=1, N=3, s=2, G=FIE, F=DR),
+]
+
+
+@pytest.mark.parametrize("p", DEGENERATE_CASES, ids=lambda p: p.label() + f"_c{p.c}")
+def test_parareal_degenerate_cases_match_oracle(p):
+    """The method's degenerate cases against the oracle at every iteration: one grid node, one
+    time slice (parareal exact after one iteration), s = 1 with F = G (Delta = 0, so U^1 = U^0
+    and the first update is 0), c = 0, and the smallest DD geometry (2 strips, 2-cell overlap)."""
+    _parareal_vs_oracle(p)
+    if p.s == 1 and p.F == p.G:
+        _, gupds = gpu_parareal(p, synth.initial_state(p), 1)
+        assert gupds[0] <= 1e-14  # (F and G may take different kernel variants: rounding only)
+
+
+def test_iterate_with_kmax_zero_keeps_the_coarse_guess():
+    """prs_iterate(kmax = 0): no iteration, k = 0, and the trajectory is the initial coarse
+    sweep U^0."""
+    prs = prs_mod()
+    p = Problem(dim=2, n=24, c=1.0, N=4, s=3, G=FIE, F=DR, init="modes", seed=1)
+    u0 = synth.initial_state(p)
+    ctx = prs.Context(p)
+    ctx.set_initial(dev(u0))
+    ctx.coarse_sweep()
+    k, hist = ctx.iterate(0, 0.0)
+    assert k == 0 and hist == []
+    buf = torch.empty((p.n, p.n), dtype=torch.float64, device="cuda")
+    traj = np.stack([host(ctx.get_slice(n, buf)).copy() for n in range(p.N + 1)])
+    ctx.close()
+    ctraj, _ = oracle.Oracle(p).parareal(u0, 0, fixed=True)
+    scale = max(float(np.max(np.abs(t))) for t in ctraj[0])
+    assert float(np.max(np.abs(traj - ctraj[0]))) / scale <= TOL
+
+
 def test_iterate_stop_rule_and_determinism():
     """prs_iterate stops at update <= tol or k = N; two runs are bitwise identical (P12)."""
     prs = prs_mod()
