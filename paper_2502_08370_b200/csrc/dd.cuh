@@ -249,6 +249,17 @@ struct DDStageArgs {
     int ntasks;
 };
 
+#ifdef PRS_DD_TIMING
+// diagnostic build only (-DPRS_DD_TIMING): per task, ns spent waiting for the forward / the
+// backward scan totals of the other row pieces, the task's duration, and the task count
+__device__ unsigned long long g_dd_timing[4];
+__device__ __forceinline__ unsigned long long dd_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // L2-scope flag hand-off between CTAs (GX): release after the CTA's total is written, acquire
 // before reading the totals of other row pieces.  A wait that outlives any legitimate one (a
 // task lasts ~0.1 ms) traps instead of hanging the device.
@@ -596,7 +607,13 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
         __syncthreads();  // every total of this piece written (and fenced)
         if (tid == 0) {
             dd_flag_release(a.gflag + 2 * tk);
+#ifdef PRS_DD_TIMING
+            const unsigned long long tw0 = dd_gtimer();
+#endif
             for (int r = 0; r < crank; ++r) dd_flag_wait(a.gflag + 2 * (task * a.CL + r));
+#ifdef PRS_DD_TIMING
+            atomicAdd(&g_dd_timing[0], dd_gtimer() - tw0);
+#endif
         }
         __syncthreads();
 #pragma unroll
@@ -692,7 +709,13 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
         __syncthreads();
         if (tid == 0) {
             dd_flag_release(a.gflag + 2 * tk + 1);
+#ifdef PRS_DD_TIMING
+            const unsigned long long tw1 = dd_gtimer();
+#endif
             for (int r = a.CL - 1; r > crank; --r) dd_flag_wait(a.gflag + 2 * (task * a.CL + r) + 1);
+#ifdef PRS_DD_TIMING
+            atomicAdd(&g_dd_timing[1], dd_gtimer() - tw1);
+#endif
         }
         __syncthreads();
 #pragma unroll
@@ -818,7 +841,16 @@ __global__ void __launch_bounds__(DD_THREADS, 2) dd_stage_kernel(DDStageArgs a) 
             __syncthreads();
             const int tk = s_task;
             if (tk >= a.ntasks) break;
+#ifdef PRS_DD_TIMING
+            const unsigned long long tt0 = dd_gtimer();
+#endif
             dd_stage_task<DR, SRC, 1>(a, sh, tk / a.CL, tk % a.CL);
+#ifdef PRS_DD_TIMING
+            if (threadIdx.x == 0) {
+                atomicAdd(&g_dd_timing[2], dd_gtimer() - tt0);
+                atomicAdd(&g_dd_timing[3], 1ull);
+            }
+#endif
         }
     } else {
         const int crank = (a.CL > 1) ? (int)cg::this_cluster().block_rank() : 0;

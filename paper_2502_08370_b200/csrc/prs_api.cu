@@ -1331,6 +1331,15 @@ static void pipe_free(prs_ctx *ctx) {
 void prs_destroy(prs_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+#ifdef PRS_DD_TIMING
+    {
+        unsigned long long h[4] = {0, 0, 0, 0};
+        cudaMemcpyFromSymbol(h, prs::g_dd_timing, sizeof(h));
+        if (h[3])
+            fprintf(stderr, "DD timing: %llu tasks, per task %.1f us, forward wait %.1f us, backward wait %.1f us\n",
+                    h[3], h[2] / 1e3 / h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3]);
+    }
+#endif
     if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
     double *bufs[] = {ctx->traj, ctx->fa, ctx->fb, ctx->gcache, ctx->gtmp, ctx->u0,
                       ctx->sinpi, ctx->s2n, ctx->s2f};
