@@ -255,6 +255,8 @@ def run_prs(args):
     if args.pipeline:
         assert args.steps <= p.N, "--pipeline: steps <= N (one prs_iterate call)"
         _, upds = ctx.iterate(args.steps, 0.0)
+        # (an exactly zero update -- finite termination -- stops the call early: the rate
+        # counts the iterations that ran)
     else:
         for _ in range(args.steps):
             upds.append(step())
@@ -275,7 +277,7 @@ def run_prs(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    total_updates = updates_per_step(p) * args.steps
+    total_updates = updates_per_step(p) * len(upds)
     value = total_updates / (ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers (rank-local, then max) ----

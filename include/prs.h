@@ -72,6 +72,17 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (call on rank 0 only). */
 int prs_nccl_unique_id(void *uid128);
 
+/* In-process multi-rank world (tests of the multi-rank driver on ONE device): nranks contexts
+ * of one process, created with prs_create_local(..., rank, world, ...) and driven by one host
+ * thread each, exchange their slice states / bands / stop-test words through device-to-device
+ * copies ordered by CUDA events and matched on the host (no kernel waits on another rank).
+ * The contexts run the same driver code as NCCL ranks (the data plane is an interface with an
+ * NCCL and this local implementation).  The world outlives its contexts; a
+ * host-side wait that is not matched within 300 s fails with PRS_ENCCL. */
+int prs_local_world_create(int nranks, void **world);
+void prs_local_world_destroy(void *world);
+int prs_create_local(const prs_problem *prob, int rank, void *world, void *cuda_stream, prs_ctx **out);
+
 /* Slices [first, first+count) owned by `rank` out of nranks (host only, no GPU needed). */
 int prs_partition(int N, int nranks, int rank, int *first, int *count);
 
@@ -91,7 +102,12 @@ int prs_fine_sweep(prs_ctx *ctx);
 int prs_parareal_correct(prs_ctx *ctx, double *update_out);
 
 /* Loop fine_sweep + parareal_correct until update <= tol or k = min(kmax, N) (finite
- * termination).  hist (kmax doubles, may be NULL) receives the updates. */
+ * termination).  hist (kmax doubles, may be NULL) receives the updates.
+ * Slices n < k are skipped at iteration k for states of >= 2^18 points (exact and bitwise
+ * frozen).  With several ranks the stop test is lagged: iteration k's all-reduce
+ * runs on a second stream / communicator while iteration k+1's fine sweep already runs (its
+ * result is discarded on a stop), so no rank waits for the last rank's chain before
+ * propagating; results are those of the unlagged loop. */
 int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist);
 
 /* Copy the current iterate U^k_n (n = 0..N) to host or device memory.  Only the rank that
@@ -145,8 +161,10 @@ int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands);
 int prs_set_pipeline(prs_ctx *ctx, int blocks);
 
 /* Host only (no GPU): the band exchange of space-parallel G for `rank` of nranks and N slices,
- * phase 0 (scatter of Delta bands from the slice owners) or 1 (gather of U / G-cache bands back
- * to them), as the point-to-point operations prs_parareal_correct issues (NCCL group).  Writes
+ * phase 0 (scatter of Delta bands from the slice owners), 1 (gather of U / G-cache bands back
+ * to them) or 2 (seed: the bands of the current iterate U^k_1..U^k_N from their owners, issued
+ * before the first band chain after set_initial / coarse_sweep / a mode switch), as the
+ * point-to-point operations prs_parareal_correct issues (NCCL group).  Writes
  * up to max_ops records of 6 ints {kind: 0 send, 1 recv, 2 local copy; what: 0 Delta_slice,
  * 1 U_{slice+1}, 2 Gcache_slice; slice; band; peer rank; owner-side local state index} to ops
  * (may be NULL) and returns the number of records, or -1 on bad arguments. */

@@ -28,7 +28,7 @@ def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(f) for f in _SRC + _HDR)
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-shared", "-fPIC",
-               "-o", _SO + ".tmp"] + _SRC + ["-lm"]
+               "-pthread", "-o", _SO + ".tmp"] + _SRC + ["-lm"]
         subprocess.check_call(cmd)
         os.replace(_SO + ".tmp", _SO)
     return _SO
@@ -66,6 +66,7 @@ def lib():
             "orc_parareal_iteration": ([P, D, D], None),
             "orc_fine_solution": ([P, D, D], None),
             "orc_nterms": ([P], I),
+            "orc_set_threads": ([I], None),
         }
         for name, (args, res) in sig.items():
             f = getattr(_lib, name)
@@ -77,6 +78,15 @@ def lib():
 def _dp(a: np.ndarray):
     assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def set_threads(k: int) -> None:
+    """Threads for the per-slice F / G evaluations of a parareal iteration (results unchanged)."""
+    lib().orc_set_threads(int(k))
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
 
 class Oracle:

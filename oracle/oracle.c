@@ -21,10 +21,16 @@
  *   - parareal           : PAPER.md:194-206, U^{k+1}_{n+1} = G(U^{k+1}_n) + F^s(U^k_n) - G(U^k_n)
  *                          evaluated left to right.
  *
- * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC (no FMA contraction).
+ * Threads: orc_set_threads(k) lets orc_parareal_iteration run its F^s(U^k_n) and G(U^k_n)
+ * evaluations -- independent per slice n ("can be computed in parallel for
+ * every n") -- on k POSIX threads, one slice per task, each with its own buffers; the values
+ * are bitwise those of the serial loop (tests/test_oracle_pins.py).  Everything else is serial.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC -pthread (no FMA contraction).
  * Parity pins for every function live in tests/test_oracle_*.py.
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 #include <stdint.h>
@@ -523,15 +529,45 @@ void orc_coarse_sweep(const orc_problem *p, const double *u0, double *traj) {
  *   U^{k+1}_0 = P u_0,
  *   U^{k+1}_{n+1} = G(U^{k+1}_n) + F^s(U^k_n) - G(U^k_n),  n = 0..N_c-1.
  * The F^s(U^k_n) are independent in n; computed serially here. */
+static int orc_threads = 1;
+void orc_set_threads(int k) { orc_threads = k < 1 ? 1 : k; }
+
+typedef struct {
+    const orc_problem *p;
+    const double *traj_k;
+    double *Fk, *Gk;
+    int next;  /* next slice to take (under lock) */
+    pthread_mutex_t lock;
+} slice_work;
+
+static void *slice_worker(void *arg) {
+    slice_work *w = (slice_work *)arg;
+    long N = npoints(w->p);
+    for (;;) {
+        pthread_mutex_lock(&w->lock);
+        int n = w->next++;
+        pthread_mutex_unlock(&w->lock);
+        if (n >= w->p->N) return NULL;
+        orc_fine(w->p, n, w->traj_k + (long)n * N, w->Fk + (long)n * N);
+        orc_coarse(w->p, n, w->traj_k + (long)n * N, w->Gk + (long)n * N);
+    }
+}
+
 void orc_parareal_iteration(const orc_problem *p, const double *traj_k, double *traj_k1) {
     long N = npoints(p);
     int Nc = p->N;
     double *Fk = malloc(sizeof(double) * N * Nc), *Gk = malloc(sizeof(double) * N * Nc);
     double *g = malloc(sizeof(double) * N);
-    for (int n = 0; n < Nc; ++n) {
-        orc_fine(p, n, traj_k + (long)n * N, Fk + (long)n * N);
-        orc_coarse(p, n, traj_k + (long)n * N, Gk + (long)n * N);
-    }
+    /* F^s(U^k_n), G(U^k_n) for every n (independent slices; serial when orc_threads == 1) */
+    slice_work w = {p, traj_k, Fk, Gk, 0};
+    pthread_mutex_init(&w.lock, NULL);
+    int nt = orc_threads < Nc ? orc_threads : Nc;
+    pthread_t th[256];
+    if (nt > 256) nt = 256;
+    for (int t = 1; t < nt; ++t) pthread_create(&th[t], NULL, slice_worker, &w);
+    slice_worker(&w);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&w.lock);
     memcpy(traj_k1, traj_k, sizeof(double) * N); /* U^{k+1}_0 = U^k_0 = P u_0 */
     for (int n = 0; n < Nc; ++n) {
         orc_coarse(p, n, traj_k1 + (long)n * N, g);

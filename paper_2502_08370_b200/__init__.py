@@ -21,7 +21,8 @@ PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
 EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
            "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_set_pipeline", "prs_gpar_plan", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
-           "prs_last_error", "prs_destroy"]
+           "prs_last_error", "prs_destroy", "prs_local_world_create", "prs_local_world_destroy",
+           "prs_create_local"]
 
 
 class PrsError(RuntimeError):
@@ -73,6 +74,9 @@ def lib() -> ctypes.CDLL:
             "prs_kernel_stats": ([V, I, PL, PD, PD], I),
             "prs_last_error": ([V], ctypes.c_char_p),
             "prs_destroy": ([V], None),
+            "prs_local_world_create": ([I, ctypes.POINTER(V)], I),
+            "prs_local_world_destroy": ([V], None),
+            "prs_create_local": ([ctypes.POINTER(prs_problem), I, V, V, ctypes.POINTER(V)], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -117,18 +121,40 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class LocalWorld:
+    """prs_local_world_create: `nranks` in-process ranks on the current device (tests of the
+    multi-rank driver; each rank's Context is driven by its own host thread)."""
+
+    def __init__(self, nranks: int):
+        self.L = lib()
+        h = ctypes.c_void_p()
+        rc = self.L.prs_local_world_create(nranks, ctypes.byref(h))
+        if rc != PRS_OK:
+            raise PrsError(rc, "prs_local_world_create failed")
+        self.h, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.prs_local_world_destroy(self.h)
+            self.h = None
+
+
 class Context:
     """One prs_ctx.  Tensors passed in must be contiguous float64 CUDA tensors (or, for the
     host-buffer calls, contiguous float64 CPU tensors / numpy arrays)."""
 
     def __init__(self, prob, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None,
-                 stream: int | None = None):
+                 stream: int | None = None, world: LocalWorld | None = None):
         self.L = lib()
         self.prob = prob
         self._cp = to_c_problem(prob)
         h = ctypes.c_void_p()
-        uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid else None
-        rc = self.L.prs_create(ctypes.byref(self._cp), rank, nranks, uid, stream, ctypes.byref(h))
+        if world is not None:
+            nranks = world.nranks
+            rc = self.L.prs_create_local(ctypes.byref(self._cp), rank, world.h, stream, ctypes.byref(h))
+        else:
+            uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid else None
+            rc = self.L.prs_create(ctypes.byref(self._cp), rank, nranks, uid, stream, ctypes.byref(h))
         if rc != PRS_OK:
             raise PrsError(rc, "prs_create failed (see stderr)")
         self.h = h
@@ -151,10 +177,27 @@ class Context:
         except Exception:
             pass
 
-    @staticmethod
-    def _ptr(x):
+    def _ptr(self, x, states: int = 1, need_cuda: bool = False):
+        """Pointer of a contiguous float64 buffer of `states` states (n^dim doubles each): a
+        torch tensor (CUDA: on the context's device; CPU) or a numpy array.  Anything else is
+        rejected here, before it can reach the ABI as a wrong-typed or wrong-sized pointer."""
+        need = states * self.prob.n ** self.prob.dim
         if hasattr(x, "data_ptr"):
+            import torch
+            if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() < need:
+                raise ValueError(f"need a contiguous float64 tensor of >= {need} elements, got "
+                                 f"{x.dtype} {tuple(x.shape)} contiguous={x.is_contiguous()}")
+            if x.is_cuda and x.device.index != torch.cuda.current_device():
+                raise ValueError(f"tensor on {x.device}, context on cuda:{torch.cuda.current_device()}")
+            if need_cuda and not x.is_cuda:
+                raise ValueError("this call takes device buffers (CUDA tensors)")
             return ctypes.c_void_p(x.data_ptr()), bool(x.is_cuda)
+        import numpy as np
+        if need_cuda:
+            raise ValueError("this call takes device buffers (CUDA tensors)")
+        if not isinstance(x, np.ndarray) or x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"] \
+                or x.size < need:
+            raise ValueError(f"need a C-contiguous float64 array of >= {need} elements")
         return ctypes.c_void_p(x.ctypes.data), False
 
     def set_initial(self, u0):
@@ -185,14 +228,14 @@ class Context:
         return out
 
     def step(self, scheme: int, tau: float, t_next: float, inp, out):
-        pi, _ = self._ptr(inp)
-        po, _ = self._ptr(out)
+        pi, _ = self._ptr(inp, need_cuda=True)
+        po, _ = self._ptr(out, need_cuda=True)
         self._check(self.L.prs_step(self.h, scheme, tau, t_next, pi, po))
         return out
 
     def step_batch(self, which: int, slice0: int, j: int, inp, out, B: int):
-        pi, _ = self._ptr(inp)
-        po, _ = self._ptr(out)
+        pi, _ = self._ptr(inp, B, need_cuda=True)
+        po, _ = self._ptr(out, B, need_cuda=True)
         self._check(self.L.prs_step_batch(self.h, which, slice0, j, pi, po, B))
         return out
 

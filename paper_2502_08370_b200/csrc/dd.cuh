@@ -882,6 +882,7 @@ struct DDData {
     int num_sms = 148;
     int *gbuf = nullptr;        // [1 + 2 * gcap]: task counter, flags
     double2 *gtot = nullptr;    // [gcap][2][DD_WMAX]
+    int gen = 0;                // bumped when gbuf / gtot are reallocated (captured graphs hold them)
     long long gcap = 0;
 };
 
@@ -1079,6 +1080,7 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
                 return PRS_ECUDA;
             }
             d.gcap = ntasks;
+            ++d.gen;
         }
         a.gctr = reinterpret_cast<unsigned *>(d.gbuf);
         a.gflag = d.gbuf + 1;

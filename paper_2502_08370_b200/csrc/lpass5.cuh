@@ -182,31 +182,6 @@ __global__ void lp5_scan_kernel(L5Args a, long long ncols) {
     }
 }
 
-// Same scan when the block tuples come from xpass6: data parts B (tt[1]) and Q (tt[3]) per
-// state, pivot-only parts A, P, R from the per-tau table apr = [3][nrb][n].
-__global__ void lp6_scan_kernel(L5Args a, const double *__restrict__ apr, long long ncols) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= ncols) return;
-    const long long sq = idx / a.n;
-    const int col = (int)(idx - sq * a.n);
-    const long long o0 = sq * a.nrb * a.n + col;
-    const long long plane = (long long)a.nrb * a.n;
-    const double *tB = a.tt + a.tstride, *tQ = a.tt + 3 * a.tstride;
-    double Y = 0.0;
-    for (int rb = 0; rb < a.nrb; ++rb) {
-        const long long o = o0 + (long long)rb * a.n;
-        a.yx[o] = Y;
-        Y = fma(__ldg(apr + (long long)rb * a.n + col), Y, tB[o]);
-    }
-    double X = 0.0;
-    for (int rb = a.nrb - 1; rb >= 0; --rb) {
-        const long long o = o0 + (long long)rb * a.n;
-        const long long to = (long long)rb * a.n + col;
-        a.yx[a.tstride + o] = X;
-        X = fma(__ldg(apr + plane + to), X, fma(__ldg(apr + 2 * plane + to), a.yx[o], tQ[o]));
-    }
-}
-
 template <int COEF, int EPI>
 __global__ void __launch_bounds__(L5T, 2) lp5_finish_kernel(L5Args a) {
     __shared__ double st[5][L5CP][L5W];

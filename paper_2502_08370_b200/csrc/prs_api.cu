@@ -24,13 +24,12 @@
 #include "lpass3.cuh"
 #include "lpass4.cuh"
 #include "lpass5.cuh"
-#include "xpass6.cuh"
 #include "lpass8.cuh"
-#include "lpass9.cuh"
 #include "xy3.cuh"
 #include "gpar.cuh"
 #include "sweep2.cuh"
 #include "xpass7.cuh"
+#include "transport.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -52,6 +51,7 @@ struct Nccl {
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
     bool load(std::string &err) {
         if (h) return true;
@@ -75,12 +75,52 @@ struct Nccl {
         SYM(AllGather, "ncclAllGather");
         SYM(GroupStart, "ncclGroupStart");
         SYM(GroupEnd, "ncclGroupEnd");
+        SYM(CommSplit, "ncclCommSplit");
         SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
         return true;
     }
 };
 Nccl g_nccl;
+
+// NCCL over NVLink / NVSwitch (transport.cuh): channel 0 = the data plane, channel 1 = a split
+// communicator for the stop-test all-reduce (its own stream in the lagged stop test)
+struct NcclTransport : Transport {
+    ncclComm_t comm[2] = {nullptr, nullptr};
+    ~NcclTransport() override {
+        for (ncclComm_t c : comm)
+            if (c && g_nccl.CommDestroy) g_nccl.CommDestroy(c);
+    }
+    int chk(ncclResult_t r, const char *what) {
+        if (r == ncclSuccess) return 0;
+        err = std::string(what) + ": " + g_nccl.GetErrorString(r);
+        return PRS_ENCCL;
+    }
+    int init(const void *uid, int nranks, int rank) {
+        if (!g_nccl.load(err)) return PRS_ENCCL;
+        ncclUniqueId id;
+        memcpy(&id, uid, sizeof(id));
+        if (int rc = chk(g_nccl.CommInitRank(&comm[0], nranks, id, rank), "ncclCommInitRank")) return rc;
+        return chk(g_nccl.CommSplit(comm[0], 0, rank, &comm[1], nullptr), "ncclCommSplit");
+    }
+    int group_start() override { return chk(g_nccl.GroupStart(), "ncclGroupStart"); }
+    int group_end() override { return chk(g_nccl.GroupEnd(), "ncclGroupEnd"); }
+    int send(const double *buf, size_t count, int peer, cudaStream_t st, int ch) override {
+        return chk(g_nccl.Send(buf, count, ncclDouble, peer, comm[ch], st), "ncclSend");
+    }
+    int recv(double *buf, size_t count, int peer, cudaStream_t st, int ch) override {
+        return chk(g_nccl.Recv(buf, count, ncclDouble, peer, comm[ch], st), "ncclRecv");
+    }
+    int allreduce_max_u64(unsigned long long *buf, size_t count, cudaStream_t st, int ch) override {
+        return chk(g_nccl.AllReduce(buf, buf, count, ncclUint64, ncclMax, comm[ch], st), "ncclAllReduce");
+    }
+    // (in place: the send buffer is this rank's segment of recv)
+    int allgather_inplace(double *recv, size_t count, cudaStream_t st, int ch) override {
+        return chk(g_nccl.AllGather(recv + (size_t)my_rank * count, recv, count, ncclDouble, comm[ch], st),
+                   "ncclAllGather");
+    }
+    int my_rank = 0;
+};
 
 }  // namespace
 
@@ -89,9 +129,6 @@ struct TauFactors {
     double tau = -1.0;
     double *tab = nullptr;               // 3 n (m, id, cc), kappa = 1
     double *invdx = nullptr, *invdy = nullptr;  // n^2 each, variable kappa
-    double *apr = nullptr;               // fused 2-D path: y block tuple constants [3][n/64][n]
-    double *ymt = nullptr, *ycid = nullptr;  // fused 2-D path: y-walk tables (n^2, or n for kappa = 1)
-    double *idxp = nullptr;              // fused 2-D path: invdx in xpass6's interleaved layout
 };
 
 struct prs_ctx {
@@ -113,6 +150,11 @@ struct prs_ctx {
     DDData dd;
     unsigned long long *red = nullptr;  // [0] update bits, [1] flag, [2] scratch
     unsigned long long *red_host = nullptr;
+    unsigned long long *red_base = nullptr;  // 8 words: [0,1] / [4,5] = (update bits, flag) of the
+                                             // two iteration parities, [2] scratch; red points at
+                                             // the current parity's pair
+    cudaStream_t ctl = nullptr;              // lagged stop test (nranks > 1): the all-reduce stream
+    cudaEvent_t ev_chain[2] = {nullptr, nullptr}, ev_red[2] = {nullptr, nullptr};
     double u0norm = 1.0;
     bool have_initial = false, have_coarse = false;
     long long launches = 0;
@@ -123,28 +165,10 @@ struct prs_ctx {
     size_t ev_used = 0;
     long long k_launch[3] = {0, 0, 0};
     double k_ms[3] = {0, 0, 0}, k_bytes[3] = {0, 0, 0};
-    ncclComm_t comm = nullptr;
+    Transport *tr = nullptr;  // nranks > 1: NCCL (prs_create) or the in-process world (prs_create_local)
     int num_sms = 148;
-    bool force_v2 = false;  // PRS_XPASS=2: use the non-persistent x-pass (A/B measurements)
-    bool force_l3 = false;  // PRS_LPASS=3: cluster pass lpass3 instead of lpass4 / lpass5
-    bool no_fused = false;  // PRS_FUSED=0: 2-D long lines take xpass3 + lpass5 (A/B measurements)
-    bool fused_notup = false;  // PRS_FUSED=2: xpass6 without the fused y tuples + lp5 tuple kernel
-    bool no_l8 = false;        // PRS_L8=0: long strided lines take lp5 (one tile per CTA) instead of lp8
-    int l8wide = 1;            // lp8 finish at 1 CTA / SM: whole register file (no coefficient spills),
-                               // 4-slot ring; PRS_L8WIDE=0: 2 CTAs / SM, 128 registers, 3 slots
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
-    bool x3_contig = false;    // PRS_X3CONTIG=1: xpass3 takes one contiguous range per CTA
     bool no_sweep2 = false;    // PRS_SWEEP2=0: small 2-D slices step through the per-step kernels
-    bool no_x7 = false;        // PRS_X7=0: 4096-point rows take xpass3 instead of the 2-CTA xpass7
-    bool x3_tma = false;       // PRS_X3TMA=1: xpass3 fills its ring by TMA tensor copies (one per
-                               // group, 128-byte swizzle) instead of 16-byte cp.async; measured
-                               // ~3% slower on c3 (the pass is bound by its row latency chain)
-    // TMA tensor maps (rows of 16 doubles, 128-byte swizzle) by (address, rows)
-    std::vector<std::pair<std::pair<const void *, long long>, CUtensorMap>> tmaps;
-    bool no_tiled = true;      // PRS_TILED=1: 2-D long lines take lp9 x tiles + lp8 (opt-in:
-                               // measured slower than xpass3 + lp8, profiles/r01_fused_notes.md)
-    double *l9buf = nullptr;   // tiled 2-D path: x / y block tuples and scan results
-    size_t l9_bytes = 0;
     // CUDA graphs of the per-iteration launch sequences (single rank, profiling off): the
     // fine sweep and the coarse correction chain are captured on their second call (the first
     // one allocates lazily-sized scratch) and replayed afterwards.  PRS_GRAPHS=0 disables.
@@ -152,16 +176,26 @@ struct prs_ctx {
     int fine_calls = 0, corr_calls = 0;
     cudaGraphExec_t fine_exec = nullptr, corr_exec = nullptr;
     long long fine_glaunch = 0, corr_glaunch = 0;  // kernels per replay
+    // captured graphs hold pointers to lazily sized scratch (l5buf, the DD exchange buffers):
+    // scratch_gen counts their reallocations; a graph captured under another generation is
+    // destroyed and captured again
+    int scratch_gen = 0;
+    int fine_gen = -1, corr_gen = -1;
     // prs_iterate: slices n < kconv are converged (U^k_n exact and bitwise frozen for n <= k,
     // PAPER.md:214), so their fine propagation and coarse correction would reproduce the
     // previous iteration's Delta_n and U_{n+1}: they are skipped.  Enabled for states of
     // >= 2^18 points (PRS_SKIP=0/1 overrides); bare fine_sweep / correct calls never skip.
     bool skip_converged = false;
     int kconv = 0;
+    bool lag = true;  // nranks > 1: prs_iterate reads the stop test one fine sweep late (PRS_LAG=0: off)
     // space-parallel G (gpar.cuh): P bands of gnb rows; one process runs all P (virtual bands)
     int gpar = 0, gP = 1, gnb = 0;
     double *gb_u = nullptr, *gb_d = nullptr, *gb_gc = nullptr;  // multi-rank: this rank's band of
                                                                  // U_0..U_N, Delta_0.., Gcache_0..
+    bool gb_valid = false;     // multi-rank: gb_u holds this rank's bands of the current iterate
+                               // U^k_1..U^k_N (the update norm of the chain's CORRECT epilogue reads
+                               // them); false after anything that writes the trajectory outside
+                               // the band chain (set_initial, coarse_sweep, a mode switch)
     double *gb_v = nullptr;    // x-stage output (a full state: P bands when virtual)
     double *gb_tt = nullptr;   // per band: block tuples [5] + scan [2] x (gnb/64) x n
     double *gb_tot = nullptr;  // band tuples [P][5][n]
@@ -192,10 +226,10 @@ struct prs_ctx {
 
 #define NK(call)                                                                 \
     do {                                                                         \
-        ncclResult_t r_ = (call);                                                \
-        if (r_ != ncclSuccess) {                                                 \
-            ctx->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);     \
-            return PRS_ENCCL;                                                    \
+        int r_ = (call);                                                         \
+        if (r_ != PRS_OK) {                                                      \
+            ctx->err = ctx->tr->err;                                             \
+            return r_;                                                           \
         }                                                                        \
     } while (0)
 
@@ -255,13 +289,6 @@ static int prof_flush(prs_ctx *ctx) {
     return PRS_OK;
 }
 
-// 2-D long lines: x-pass with fused y block tuples (xpass6) + tuple scan + lp5 finish
-static bool fused2d_ok(const prs_ctx *ctx) {
-    const int n = ctx->p.n;
-    return !ctx->no_fused && !ctx->force_v2 && !ctx->force_l3 && ctx->p.dim == 2 && ctx->p.split == 0 &&
-           (n == 1024 || n == 2048 || n == 4096);
-}
-
 // ------------------------------------------------------------------ factors --------
 static int ensure_factors(prs_ctx *ctx, int slot, double tau) {
     TauFactors &f = ctx->fac[slot];
@@ -286,24 +313,6 @@ static int ensure_factors(prs_ctx *ctx, int slot, double tau) {
                                                     ctx->s2f, f.invdy);
         TRY(last_launch(ctx));
     }
-    if (fused2d_ok(ctx)) {
-        const int nrb = n / X6RB;
-        const size_t tl = ctx->p.coef_kind ? (size_t)n * n : (size_t)n;
-        if (!f.apr) CK(cudaMalloc(&f.apr, sizeof(double) * 3 * (size_t)nrb * n));
-        if (!f.ymt) CK(cudaMalloc(&f.ymt, sizeof(double) * tl));
-        if (!f.ycid) CK(cudaMalloc(&f.ycid, sizeof(double) * tl));
-        const long long cnt = (long long)nrb * n;
-        setup_ytuple_tab<<<(unsigned)((cnt + 127) / 128), 128, 0, ctx->stream>>>(
-            n, ctx->p.coef_kind, tau, ctx->h2inv, CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr},
-            f.invdy, ctx->s2n, ctx->s2f, f.apr, f.ymt, f.ycid);
-        TRY(last_launch(ctx));
-        if (ctx->p.coef_kind) {
-            if (!f.idxp) CK(cudaMalloc(&f.idxp, sizeof(double) * (size_t)n * n));
-            const long long nn = (long long)n * n;
-            x6_permute_rows<<<(unsigned)((nn + 255) / 256), 256, 0, ctx->stream>>>(f.invdx, f.idxp, n);
-            TRY(last_launch(ctx));
-        }
-    }
     return PRS_OK;
 }
 
@@ -316,51 +325,9 @@ struct EpiArgs {
     double *traj = nullptr;
 };
 
-// ---- TMA tensor maps: a buffer of `rows` x 16 doubles (128-byte rows), box 16 x 256
-// (one 4096-double group), 128-byte swizzle; encoded through the driver entry point (no
-// link-time libcuda dependency) and cached per (address, rows)
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static int get_tmap(prs_ctx *ctx, const void *ptr, long long rows, CUtensorMap *out) {
-    for (auto &e : ctx->tmaps)
-        if (e.first.first == ptr && e.first.second == rows) {
-            *out = e.second;
-            return PRS_OK;
-        }
-    static PFN_encodeTiled encode = nullptr;
-    if (!encode) {
-        void *fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) {
-            ctx->err = "cuTensorMapEncodeTiled unavailable";
-            return PRS_ECUDA;
-        }
-        encode = reinterpret_cast<PFN_encodeTiled>(fn);
-    }
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {(cuuint64_t)LCH, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)(LCH * sizeof(double))};
-    const cuuint32_t box[2] = {(cuuint32_t)LCH, (cuuint32_t)X3T};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptr), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        ctx->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
-        return PRS_ECUDA;
-    }
-    if (ctx->tmaps.size() > 64) ctx->tmaps.clear();
-    ctx->tmaps.push_back({{ptr, rows}, m});
-    *out = m;
-    return PRS_OK;
-}
-
 // persistent pipelined x-pass (xpass3.cuh) when the shape allows it
 static bool xpass3_ok(const prs_ctx *ctx, long long B) {
     const int n = ctx->p.n;
-    if (ctx->force_v2) return false;
     if (n < 16 || n > 4096 || (n & (n - 1)) != 0) return false;
     const long long lines = B * (ctx->p.dim == 2 ? (long long)n : (long long)n * n);
     const int lpg = 4096 / n;
@@ -384,7 +351,7 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     // state-fastest ranges when every state has enough groups: the number of ranges makes
     // B * nranges a multiple of the grid (balanced), each range >= 64 groups
     a.nranges = 0;
-    if (!ctx->x3_contig && B > 1) {
+    if (B > 1) {
         const long long grid = std::min<long long>(ctx->num_sms, a.ngroups);
         long long g = grid, bb = B;
         while (bb) { const long long t = g % bb; g = bb; bb = t; }  // gcd(grid, B)
@@ -405,16 +372,9 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     const int dr = (scheme == PRS_DR) ? 1 : 0;
     const int coef = ctx->p.coef_kind;
     const int src = ctx->p.source_kind;
-    const size_t shm = xpass3_smem_bytes(coef, ctx->x3_tma ? 1 : 0);
+    const size_t shm = xpass3_smem_bytes(coef);
     void (*kern)(X3Args) = nullptr;
-    const int tma = ctx->x3_tma ? 1 : 0;
-    if (tma) {
-        TRY(get_tmap(ctx, in, B * ctx->vol / LCH, &a.tm_in));
-        if (coef) TRY(get_tmap(ctx, f.invdx, (long long)n * n / LCH, &a.tm_piv));
-    }
-#define XK(C, D, S_)                                                                 \
-    if (coef == C && dr == D && src == S_)                                           \
-        kern = tma ? xpass3_kernel<C, D, S_, 1> : xpass3_kernel<C, D, S_, 0>;
+#define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass3_kernel<C, D, S_>;
     XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
 #undef XK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -437,7 +397,7 @@ static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.nstates = (int)B;
     const long long ncl = ctx->num_sms;  // one cluster per SM pair slot: 2 CTAs per SM
     a.nranges = 0;
-    if (!ctx->x3_contig && B > 1) {
+    if (B > 1) {
         long long g = ncl, bb = B;
         while (bb) { const long long t = g % bb; g = bb; bb = t; }
         const long long R = ncl / g;
@@ -481,7 +441,7 @@ static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const do
 
 static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
                         long long B, const TimeArgs &ta, bool prof) {
-    if (!ctx->no_x7 && !ctx->force_v2 && ctx->p.dim == 2 && ctx->p.n == X7N && ctx->ss == ctx->vol)
+    if (ctx->p.dim == 2 && ctx->p.n == X7N && ctx->ss == ctx->vol)
         return launch_xpass7(ctx, scheme, f, in, out, B, ta, prof);
     if (xpass3_ok(ctx, B)) return launch_xpass3(ctx, scheme, f, in, out, B, ta, prof);
     const int n = ctx->p.n, dim = ctx->p.dim;
@@ -567,8 +527,7 @@ static int launch_lpass3(prs_ctx *ctx, int axis, const TauFactors &f, const doub
     const int coef = ctx->p.coef_kind;
     // clusters (long lines): one exchange of composed tuples per panel, hidden behind the
     // previous panel (lpass4); single-CTA lines: lpass3
-    const bool use4 = a.CL > 1 && !ctx->force_l3;
-    a.noex = getenv("PRS_EXP_NOEX") ? 1 : 0;
+    const bool use4 = a.CL > 1;
     const size_t shm = use4 ? lpass4_smem_bytes(a.PW, a.R, a.CL, coef) : lpass3_smem_bytes(a.PW, a.R, a.CL, coef);
     void (*kern)(L3Args) = nullptr;
 #define LK(W, C, E)                                                   \
@@ -610,11 +569,10 @@ static int launch_lpass3(prs_ctx *ctx, int axis, const TauFactors &f, const doub
 
 // long strided lines (n >= 2048): tuple / scan / finish over 64 x 64 tiles (lpass5.cuh)
 // the lp8 finish instantiation for a coefficient kind, epilogue and register width
-static void (*lp8_finish_fn(int coef, int kind, int wide))(L5Args) {
+static void (*lp8_finish_fn(int coef, int kind))(L5Args) {
     void (*f8)(L5Args) = nullptr;
-#define LK(C, E, W) if (coef == C && kind == E && wide == W) f8 = lp8_kernel<C, E, 1, W>;
-    LK(0, 0, 0) LK(0, 1, 0) LK(0, 2, 0) LK(0, 3, 0) LK(1, 0, 0) LK(1, 1, 0) LK(1, 2, 0) LK(1, 3, 0)
-    LK(0, 0, 1) LK(0, 1, 1) LK(0, 2, 1) LK(0, 3, 1) LK(1, 0, 1) LK(1, 1, 1) LK(1, 2, 1) LK(1, 3, 1)
+#define LK(C, E) if (coef == C && kind == E) f8 = lp8_kernel<C, E, 1, 1>;
+    LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
 #undef LK
     return f8;
 }
@@ -652,6 +610,7 @@ static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const doub
         ctx->l5buf = nullptr;
         CK(cudaMalloc(&ctx->l5buf, need));
         ctx->l5_bytes = need;
+        ++ctx->scratch_gen;
     }
     a.tt = ctx->l5buf;
     a.yx = ctx->l5buf + 5 * a.tstride;
@@ -667,7 +626,7 @@ static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const doub
     LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
 #undef LK
     const long long ncols = B * a.nq * (long long)n;
-    const bool use8 = !ctx->no_l8 && a.nq == 1;
+    const bool use8 = a.nq == 1;
     if (prof) TRY(prof_begin(ctx));
     if (use8) {
         // persistent over slice groups: coefficients once per tile position, state tiles
@@ -676,9 +635,9 @@ static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const doub
         a.s8 = (int)std::min<long long>(B, 16);
         a.nsg8 = (int)((B + a.s8 - 1) / a.s8);
         const long long grid = (long long)a.nrb * a.ncb * a.nsg8;
-        const size_t shm = lpass8_smem_bytes(0), shmf = lpass8_smem_bytes(ctx->l8wide);
+        const size_t shm = lpass8_smem_bytes(0), shmf = lpass8_smem_bytes(1);
         void (*t8)(L5Args) = coef ? lp8_kernel<1, 0, 0> : lp8_kernel<0, 0, 0>;
-        void (*f8)(L5Args) = lp8_finish_fn(coef, ep.kind, ctx->l8wide);
+        void (*f8)(L5Args) = lp8_finish_fn(coef, ep.kind);
         CK(cudaFuncSetAttribute(t8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
         CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmf));
         t8<<<(unsigned)grid, L5T, shm, ctx->stream>>>(a);
@@ -707,9 +666,9 @@ static int launch_lpass5(prs_ctx *ctx, int axis, const TauFactors &f, const doub
 static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const double *in, double *out,
                         long long B, const EpiArgs &ep, bool prof) {
     const int n = ctx->p.n, dim = ctx->p.dim;
-    if (!ctx->force_v2 && !ctx->force_l3 && n >= 2048 && n <= 4096 && (n & (n - 1)) == 0)
+    if (n >= 2048 && n <= 4096 && (n & (n - 1)) == 0)
         return launch_lpass5(ctx, axis, f, in, out, B, ep, prof);
-    if (!ctx->force_v2 && n >= 64 && n <= 4096 && (n & (n - 1)) == 0)
+    if (n >= 64 && n <= 4096 && (n & (n - 1)) == 0)
         return launch_lpass3(ctx, axis, f, in, out, B, ep, prof);
     LArgs a{};
     a.in = in;
@@ -782,256 +741,6 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
     return PRS_OK;
 }
 
-static int l5_buffers(prs_ctx *ctx, long long tstride) {
-    const size_t need = sizeof(double) * 7 * (size_t)tstride;
-    if (ctx->l5_bytes < need) {
-        if (ctx->l5buf) CK(cudaFree(ctx->l5buf));
-        ctx->l5buf = nullptr;
-        CK(cudaMalloc(&ctx->l5buf, need));
-        ctx->l5_bytes = need;
-    }
-    return PRS_OK;
-}
-
-// fused 2-D step: xpass6 (x solve + y block tuples), lp6_scan, lp5_finish (y solve + epilogue)
-static int launch_fused2d(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out, long long B,
-                          const TimeArgs &ta, const EpiArgs &ep, bool prof, long long stride) {
-    const int n = ctx->p.n;
-    const int nrb = n / X6RB;
-    const long long tstride = B * (long long)nrb * n;
-    TRY(l5_buffers(ctx, tstride));
-    X6Args x{};
-    x.in = in;
-    x.out = out;
-    x.vol = stride;
-    x.n = n;
-    x.B = (int)B;
-    x.nrb = nrb;
-    const int per_sm = 4096 / n;  // CTAs per SM (512 threads of 128 registers per SM)
-    const long long ctas = (long long)ctx->num_sms * per_sm;
-    // two tuple blocks per unit (fewer halo rows) when there is enough work for every CTA
-    x.ub = (B * nrb / 2 >= 4 * ctas) ? 2 : 1;
-    x.nunits = (int)(B * nrb / x.ub);
-    x.tau = f.tau;
-    x.h2inv = ctx->h2inv;
-    x.creact = ctx->creact;
-    x.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
-    x.sinpi = ctx->sinpi;
-    x.ta = ta;
-    x.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
-    x.invdx = f.idxp;
-    x.ymt = f.ymt;
-    x.ycid = f.ycid;
-    x.s2n = ctx->s2n;
-    x.s2f = ctx->s2f;
-    x.ttB = ctx->l5buf + tstride;
-    x.ttQ = ctx->l5buf + 3 * tstride;
-    const int coef = ctx->p.coef_kind, dr = (scheme == PRS_DR) ? 1 : 0, src = ctx->p.source_kind;
-    void (*kx)(X6Args) = nullptr;
-    const int tup = ctx->fused_notup ? 0 : 1;
-#define XK(NT, C, D, S_)                                                                              \
-    if (n == NT * X6C && coef == C && dr == D && src == S_)                                           \
-        kx = tup ? xpass6_kernel<NT, C, D, S_, 1> : xpass6_kernel<NT, C, D, S_, 0>;
-#define XKN(NT) XK(NT, 0, 0, 0) XK(NT, 0, 0, 1) XK(NT, 0, 1, 0) XK(NT, 0, 1, 1) XK(NT, 1, 0, 0) XK(NT, 1, 0, 1) XK(NT, 1, 1, 0) XK(NT, 1, 1, 1)
-    XKN(128) XKN(256) XKN(512)
-#undef XKN
-#undef XK
-    if (!kx) {
-        ctx->err = "xpass6: unsupported shape";
-        return PRS_EUNSUPPORTED;
-    }
-    const size_t shm = xpass6_smem_bytes(n);
-    CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    const long long grid = std::min<long long>(ctas, x.nunits);
-    if (prof) TRY(prof_begin(ctx));
-    kx<<<(unsigned)grid, n / X6C, shm, ctx->stream>>>(x);
-    TRY(last_launch(ctx));
-    if (prof) {
-        // state read + write, the block tuples written, the factor tables (x pivots, y-walk m
-        // and cp id: read once per launch, shared by the B states)
-        const double bytes = (double)B * ctx->vol * (16.0 + 16.0 / X6RB) + (coef ? 24.0 * ctx->vol : 0.0);
-        TRY(prof_end(ctx, PRS_K_XPASS, bytes));
-    }
-    // y stage
-    L5Args a{};
-    a.in = out;
-    a.out = out;
-    a.vol = stride;
-    a.n = n;
-    a.Sl = n;
-    a.nq = 1;
-    a.Sq = (long long)n * n;
-    a.nrb = nrb;
-    a.ncb = n / L5W;
-    a.nsq = B;
-    a.order = 1;
-    a.ntiles = B * a.nrb * a.ncb;
-    a.tau = f.tau;
-    a.h2inv = ctx->h2inv;
-    a.tab = x.tab;
-    a.invd = f.invdy;
-    a.s2n = ctx->s2n;
-    a.s2f = ctx->s2f;
-    a.tstride = tstride;
-    a.tt = ctx->l5buf;
-    a.yx = ctx->l5buf + 5 * tstride;
-    a.e_gc = ep.gc;
-    a.e_gcache = ep.gcache;
-    a.e_delta = ep.delta;
-    a.e_traj = ep.traj;
-    a.e_red = ctx->red;
-    void (*k3)(L5Args) = nullptr;
-#define LK(C, E) if (coef == C && ep.kind == E) k3 = lp5_finish_kernel<C, E>;
-    LK(0, 0) LK(0, 1) LK(0, 2) LK(0, 3) LK(1, 0) LK(1, 1) LK(1, 2) LK(1, 3)
-#undef LK
-    const long long ncols = B * (long long)n;
-    if (prof) TRY(prof_begin(ctx));
-    if (tup) {
-        lp6_scan_kernel<<<(unsigned)((ncols + 127) / 128), 128, 0, ctx->stream>>>(a, f.apr, ncols);
-        TRY(last_launch(ctx));
-    } else {
-        (coef ? lp5_tuples_kernel<1> : lp5_tuples_kernel<0>)<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
-        TRY(last_launch(ctx));
-        lp5_scan_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, ctx->stream>>>(a, ncols);
-        TRY(last_launch(ctx));
-    }
-    k3<<<(unsigned)a.ntiles, L5T, 0, ctx->stream>>>(a);
-    TRY(last_launch(ctx));
-    if (prof) {
-        // block tuples read (B, Q) + y/x written and read back (scan), state read + write,
-        // the Delta epilogue's G cache, the pivot table (once per launch)
-        double per = 16.0 + 6.0 * 8.0 / X6RB;
-        if (ep.kind == EPI_DELTA) per += 8.0;
-        const double bytes = (double)B * ctx->vol * per + (coef ? 8.0 * ctx->vol : 0.0);
-        TRY(prof_end(ctx, PRS_K_LPASS, bytes));
-    }
-    return PRS_OK;
-}
-
-// 2-D long lines (n = 2048 / 4096): both stages as 64 x 64 tile kernels persistent over slice
-// groups: x tuples (lp9 MODE 0), x scan, x finish + y tuples (lp9 MODE 1) -> r_2 in `out`,
-// y scan, y finish + epilogue (lp8 MODE 1) in place.
-static bool tiled2d_ok(const prs_ctx *ctx) {
-    const int n = ctx->p.n;
-    return !ctx->no_tiled && fused2d_ok(ctx) == false && !ctx->force_v2 && !ctx->force_l3 && !ctx->no_l8 &&
-           ctx->p.dim == 2 && ctx->p.split == 0 && (n == 2048 || n == 4096);
-}
-
-static int launch_tiled2d(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out, long long B,
-                          const TimeArgs &ta, const EpiArgs &ep, bool prof, long long stride) {
-    const int n = ctx->p.n;
-    const int nb = n / L5W;  // blocks per line (square tiles: nrb = ncb)
-    const long long ts = B * (long long)nb * n;
-    const size_t need = sizeof(double) * 14 * (size_t)ts;  // 5 + 2 (x), 5 + 2 (y)
-    if (ctx->l9_bytes < need) {
-        if (ctx->l9buf) CK(cudaFree(ctx->l9buf));
-        ctx->l9buf = nullptr;
-        CK(cudaMalloc(&ctx->l9buf, need));
-        ctx->l9_bytes = need;
-    }
-    double *ttx = ctx->l9buf, *yxx = ttx + 5 * ts, *tty = yxx + 2 * ts, *yxy = tty + 5 * ts;
-    const int coef = ctx->p.coef_kind, dr = (scheme == PRS_DR) ? 1 : 0, src = ctx->p.source_kind;
-    const CoefTab tab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
-    L9Args x{};
-    x.in = in;
-    x.out = out;
-    x.vol = stride;
-    x.n = n;
-    x.nrb = nb;
-    x.ncb = nb;
-    x.nsq = B;
-    x.s8 = (int)std::min<long long>(B, 16);
-    x.nsg8 = (int)((B + x.s8 - 1) / x.s8);
-    x.tau = f.tau;
-    x.h2inv = ctx->h2inv;
-    x.creact = ctx->creact;
-    x.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
-    x.sinpi = ctx->sinpi;
-    x.ta = ta;
-    x.tab = tab;
-    x.invdx = f.invdx;
-    x.invdy = f.invdy;
-    x.s2n = ctx->s2n;
-    x.s2f = ctx->s2f;
-    x.ttx = ttx;
-    x.yxx = yxx;
-    x.tsx = ts;
-    x.tty = tty;
-    x.tsy = ts;
-    void (*k0)(L9Args) = nullptr;
-    void (*k1)(L9Args) = nullptr;
-#define XK(C, D, S_)                                   \
-    if (coef == C && dr == D && src == S_) {           \
-        k0 = lp9_kernel<C, D, S_, 0>;                  \
-        k1 = lp9_kernel<C, D, S_, 1>;                  \
-    }
-    XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
-#undef XK
-    const size_t shm9 = lpass9_smem_bytes();
-    CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm9));
-    CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm9));
-    const long long grid = (long long)nb * nb * x.nsg8;
-    // scans: lines of nb blocks, n lines per state
-    L5Args sx{};
-    sx.n = n;
-    sx.nrb = nb;
-    sx.tt = ttx;
-    sx.yx = yxx;
-    sx.tstride = ts;
-    const long long nlines = B * (long long)n;
-    if (prof) TRY(prof_begin(ctx));
-    k0<<<(unsigned)grid, L5T, shm9, ctx->stream>>>(x);
-    TRY(last_launch(ctx));
-    lp5_scan_kernel<<<(unsigned)((nlines + 255) / 256), 256, 0, ctx->stream>>>(sx, nlines);
-    TRY(last_launch(ctx));
-    k1<<<(unsigned)grid, L5T, shm9, ctx->stream>>>(x);
-    TRY(last_launch(ctx));
-    if (prof) TRY(prof_end(ctx, PRS_K_XPASS, (double)B * (double)ctx->vol * (16.0 + (coef ? 8.0 : 0.0))));
-    // y stage
-    L5Args a{};
-    a.in = out;
-    a.out = out;
-    a.vol = stride;
-    a.n = n;
-    a.Sl = n;
-    a.nq = 1;
-    a.Sq = (long long)n * n;
-    a.nrb = nb;
-    a.ncb = nb;
-    a.nsq = B;
-    a.ntiles = B * nb * nb;
-    a.tau = f.tau;
-    a.h2inv = ctx->h2inv;
-    a.tab = tab;
-    a.invd = f.invdy;
-    a.s2n = ctx->s2n;
-    a.s2f = ctx->s2f;
-    a.tstride = ts;
-    a.tt = tty;
-    a.yx = yxy;
-    a.e_gc = ep.gc;
-    a.e_gcache = ep.gcache;
-    a.e_delta = ep.delta;
-    a.e_traj = ep.traj;
-    a.e_red = ctx->red;
-    a.s8 = x.s8;
-    a.nsg8 = x.nsg8;
-    void (*f8)(L5Args) = lp8_finish_fn(coef, ep.kind, ctx->l8wide);
-    const size_t shm8 = lpass8_smem_bytes(ctx->l8wide);
-    CK(cudaFuncSetAttribute(f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm8));
-    if (prof) TRY(prof_begin(ctx));
-    lp5_scan_kernel<<<(unsigned)((nlines + 255) / 256), 256, 0, ctx->stream>>>(a, nlines);
-    TRY(last_launch(ctx));
-    f8<<<(unsigned)grid, L5T, shm8, ctx->stream>>>(a);
-    TRY(last_launch(ctx));
-    if (prof) {
-        double per = 16.0 + (coef ? 8.0 : 0.0);
-        if (ep.kind == EPI_DELTA) per += 8.0;
-        TRY(prof_end(ctx, PRS_K_LPASS, (double)B * (double)ctx->vol * per));
-    }
-    return PRS_OK;
-}
-
 // One step of `scheme` on B consecutive states: in -> out (out holds the result, or the
 // epilogue consumes it).  tmp must be distinct from in when scheme is DR.
 static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
@@ -1040,14 +749,11 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
         return dd_step(ctx->dd, scheme, (int)(&f - ctx->fac), in, out, B, ta, ep.kind, ep.gc, ep.gcache,
                        ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err, ctx->launches,
                        2.0 * M_PI * M_PI + ctx->p.c - 1.0, ctx->p.source_kind);
-    if (fused2d_ok(ctx)) return launch_fused2d(ctx, scheme, f, in, out, B, ta, ep, prof, stride);
-    if (tiled2d_ok(ctx)) return launch_tiled2d(ctx, scheme, f, in, out, B, ta, ep, prof, stride);
     if (stride != ctx->vol) {
         ctx->err = "internal: padded slice stride on a path without stride support";
         return PRS_EUNSUPPORTED;
     }
-    if (ctx->p.dim == 3 && ctx->p.n == XY_N && ctx->p.coef_kind == 0 && scheme == PRS_FIE && !ctx->no_xy &&
-        !ctx->force_v2) {
+    if (ctx->p.dim == 3 && ctx->p.n == XY_N && ctx->p.coef_kind == 0 && scheme == PRS_FIE && !ctx->no_xy) {
         // x and y stages fused per z-plane (xy3.cuh), then the z stage
         XYArgs x{};
         x.in = in;
@@ -1154,20 +860,13 @@ static int validate(const prs_problem *p, std::string &err) {
 
 void prs_destroy(prs_ctx *ctx);
 
-int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_uid, void *cuda_stream,
-               prs_ctx **out) {
-    if (!out) return PRS_EINVAL;
-    *out = nullptr;
-    std::string verr;
-    int rc = validate(prob, verr);
-    if (rc != PRS_OK) {
-        fprintf(stderr, "prs_create: %s\n", verr.c_str());
-        return rc;
-    }
-    int first = 0, count = 0;
-    if (prs_partition(prob->N, nranks, rank, &first, &count) != PRS_OK) return PRS_EINVAL;
-    if (nranks > 1 && !nccl_uid) return PRS_EINVAL;
+// the context on `rank` of `nranks`, exchanging through `tr` (owned; nranks > 1)
+static int create_impl(const prs_problem *prob, int rank, int nranks, Transport *tr, void *cuda_stream,
+                       prs_ctx **out) {
     prs_ctx *ctx = new prs_ctx();
+    ctx->tr = tr;
+    int first = 0, count = 0;
+    prs_partition(prob->N, nranks, rank, &first, &count);
     ctx->p = *prob;
     ctx->rank = rank;
     ctx->nranks = nranks;
@@ -1197,36 +896,16 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
     CKC(cudaGetDevice(&ctx->device));
     CKC(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     {
-        const char *xv = getenv("PRS_XPASS");
-        ctx->force_v2 = xv && xv[0] == '2';
-        const char *lv = getenv("PRS_LPASS");
-        ctx->force_l3 = lv && lv[0] == '3';
-        // fused long-line path (xpass6) is opt-in: PRS_FUSED=1 (y tuples fused into the x pass)
-        // or 2 (x pass alone + lp5 tuple kernel); measured no faster than xpass3 + lpass5 on c3
-        // (profiles/r01_fused_notes.md), so the default stays on the latter
-        const char *fv = getenv("PRS_FUSED");
-        ctx->no_fused = !(fv && (fv[0] == '1' || fv[0] == '2'));
-        ctx->fused_notup = fv && fv[0] == '2';
-        const char *l8 = getenv("PRS_L8");
-        ctx->no_l8 = l8 && l8[0] == '0';
-        const char *l8w = getenv("PRS_L8WIDE");
-        ctx->l8wide = (l8w && l8w[0] == '0') ? 0 : 1;
-        const char *x7v = getenv("PRS_X7");
-        ctx->no_x7 = x7v && x7v[0] == '0';
-        const char *xbv = getenv("PRS_X3TMA");
-        ctx->x3_tma = xbv && xbv[0] == '1';
         const char *swv = getenv("PRS_SWEEP2");
         ctx->no_sweep2 = swv && swv[0] == '0';
-        const char *x3c = getenv("PRS_X3CONTIG");
-        ctx->x3_contig = x3c && x3c[0] == '1';
         const char *xyv = getenv("PRS_XY");
         ctx->no_xy = xyv && xyv[0] == '0';
         const char *sv = getenv("PRS_SKIP");
         ctx->skip_converged = sv ? (sv[0] == '1') : (ctx->vol >= (1LL << 18));
+        const char *lg = getenv("PRS_LAG");
+        ctx->lag = !(lg && lg[0] == '0');
         const char *gv = getenv("PRS_GRAPHS");
         ctx->graphs = !(gv && gv[0] == '0');
-        const char *l9 = getenv("PRS_TILED");
-        ctx->no_tiled = !(l9 && l9[0] == '1');
     }
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;
@@ -1236,15 +915,7 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         CKC(cudaStreamCreate(&ctx->stream));
         ctx->own_stream = true;
     }
-    // Fused long-line path: the batch is processed slice-fastest (every slice at the same row
-    // at once, so the factor tables are shared through L2).  States of 2^23..2^27 bytes would
-    // then put all concurrent accesses on the same L2 slices (the slice hash ignores address
-    // bits >= 28), so consecutive states are padded by 32 KB + 256 B (PRS_PAD=0 disables).
     ctx->ss = ctx->vol;
-    if (fused2d_ok(ctx)) {
-        const char *pv = getenv("PRS_PAD");
-        if (!(pv && pv[0] == '0')) ctx->ss = ctx->vol + 4128;
-    }
     const size_t sb = sizeof(double) * (size_t)ctx->ss;
     CKC(cudaMalloc(&ctx->traj, sb * (count + 1)));
     CKC(cudaMalloc(&ctx->fa, sb * count));
@@ -1255,8 +926,9 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
     CKC(cudaMalloc(&ctx->sinpi, sizeof(double) * n));
     CKC(cudaMalloc(&ctx->s2n, sizeof(double) * n));
     CKC(cudaMalloc(&ctx->s2f, sizeof(double) * (n + 1)));
-    CKC(cudaMalloc(&ctx->red, sizeof(unsigned long long) * 4));
-    CKC(cudaMallocHost(&ctx->red_host, sizeof(unsigned long long) * 4));
+    CKC(cudaMalloc(&ctx->red_base, sizeof(unsigned long long) * 8));
+    CKC(cudaMallocHost(&ctx->red_host, sizeof(unsigned long long) * 8));
+    ctx->red = ctx->red_base;
     setup_sines<<<(n + 1 + 255) / 256, 256, 0, ctx->stream>>>(n, ctx->h, ctx->sinpi, ctx->s2n, ctx->s2f);
     ctx->launches++;
     CKC(cudaGetLastError());
@@ -1278,27 +950,55 @@ int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_u
         *out = nullptr;
         return frc;
     }
-    if (nranks > 1) {
-        std::string e;
-        if (!g_nccl.load(e)) {
-            fprintf(stderr, "prs_create: %s\n", e.c_str());
-            prs_destroy(ctx);
-            *out = nullptr;
-            return PRS_ENCCL;
-        }
-        ncclUniqueId id;
-        memcpy(&id, nccl_uid, sizeof(id));
-        if (g_nccl.CommInitRank(&ctx->comm, nranks, id, rank) != ncclSuccess) {
-            fprintf(stderr, "prs_create: ncclCommInitRank failed\n");
-            ctx->comm = nullptr;
-            prs_destroy(ctx);
-            *out = nullptr;
-            return PRS_ENCCL;
-        }
-    }
     CKC(cudaStreamSynchronize(ctx->stream));
 #undef CKC
     return PRS_OK;
+}
+
+static int precreate(const prs_problem *prob, int rank, int nranks, prs_ctx **out) {
+    if (!out) return PRS_EINVAL;
+    *out = nullptr;
+    std::string verr;
+    int rc = validate(prob, verr);
+    if (rc != PRS_OK) {
+        fprintf(stderr, "prs_create: %s\n", verr.c_str());
+        return rc;
+    }
+    int first = 0, count = 0;
+    if (prs_partition(prob->N, nranks, rank, &first, &count) != PRS_OK) return PRS_EINVAL;
+    return PRS_OK;
+}
+
+int prs_create(const prs_problem *prob, int rank, int nranks, const void *nccl_uid, void *cuda_stream,
+               prs_ctx **out) {
+    TRY(precreate(prob, rank, nranks, out));
+    if (nranks > 1 && !nccl_uid) return PRS_EINVAL;
+    NcclTransport *tr = nullptr;
+    if (nranks > 1) {
+        tr = new NcclTransport();
+        tr->my_rank = rank;
+        if (tr->init(nccl_uid, nranks, rank) != PRS_OK) {
+            fprintf(stderr, "prs_create: %s\n", tr->err.c_str());
+            delete tr;
+            return PRS_ENCCL;
+        }
+    }
+    return create_impl(prob, rank, nranks, tr, cuda_stream, out);
+}
+
+int prs_local_world_create(int nranks, void **world) {
+    if (!world || nranks < 1) return PRS_EINVAL;
+    *world = new LocalWorld(nranks);
+    return PRS_OK;
+}
+
+void prs_local_world_destroy(void *world) { delete static_cast<LocalWorld *>(world); }
+
+int prs_create_local(const prs_problem *prob, int rank, void *world, void *cuda_stream, prs_ctx **out) {
+    if (!world) return PRS_EINVAL;
+    LocalWorld *w = static_cast<LocalWorld *>(world);
+    TRY(precreate(prob, rank, w->P, out));
+    return create_impl(prob, rank, w->P, w->P > 1 ? new LocalTransport(w, rank) : nullptr, cuda_stream, out);
 }
 
 static void pipe_free(prs_ctx *ctx) {
@@ -1340,7 +1040,7 @@ void prs_destroy(prs_ctx *ctx) {
                     h[3], h[2] / 1e3 / h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3]);
     }
 #endif
-    if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+    delete ctx->tr;
     double *bufs[] = {ctx->traj, ctx->fa, ctx->fb, ctx->gcache, ctx->gtmp, ctx->u0,
                       ctx->sinpi, ctx->s2n, ctx->s2f};
     for (double *b : bufs)
@@ -1349,16 +1049,17 @@ void prs_destroy(prs_ctx *ctx) {
         if (f.tab) cudaFree(f.tab);
         if (f.invdx) cudaFree(f.invdx);
         if (f.invdy) cudaFree(f.invdy);
-        if (f.apr) cudaFree(f.apr);
-        if (f.ymt) cudaFree(f.ymt);
-        if (f.idxp) cudaFree(f.idxp);
-        if (f.ycid) cudaFree(f.ycid);
     }
     dd_free(ctx->dd);
-    if (ctx->red) cudaFree(ctx->red);
+    if (ctx->red_base) cudaFree(ctx->red_base);
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
+    if (ctx->ctl) {
+        cudaStreamSynchronize(ctx->ctl);
+        cudaStreamDestroy(ctx->ctl);
+    }
+    for (cudaEvent_t e : {ctx->ev_chain[0], ctx->ev_chain[1], ctx->ev_red[0], ctx->ev_red[1]})
+        if (e) cudaEventDestroy(e);
     if (ctx->l5buf) cudaFree(ctx->l5buf);
-    if (ctx->l9buf) cudaFree(ctx->l9buf);
     if (ctx->fine_exec) cudaGraphExecDestroy(ctx->fine_exec);
     {
         double *gb[] = {ctx->gb_u, ctx->gb_d, ctx->gb_gc, ctx->gb_v, ctx->gb_tt, ctx->gb_tot, ctx->gb_yx};
@@ -1379,10 +1080,10 @@ int prs_set_initial(prs_ctx *ctx, const double *u0, int u0_on_device) {
     CK(cudaMemcpyAsync(ctx->u0, u0, ctx->sbytes, u0_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        ctx->stream));
     if (ctx->rank == 0) CK(cudaMemcpyAsync(ctx->traj, ctx->u0, ctx->sbytes, cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(cudaMemsetAsync(ctx->red + 2, 0, sizeof(unsigned long long), ctx->stream));
-    absmax_kernel<<<148 * 4, 256, 0, ctx->stream>>>(ctx->u0, ctx->vol, ctx->red + 2);
+    CK(cudaMemsetAsync(ctx->red_base + 2, 0, sizeof(unsigned long long), ctx->stream));
+    absmax_kernel<<<148 * 4, 256, 0, ctx->stream>>>(ctx->u0, ctx->vol, ctx->red_base + 2);
     TRY(last_launch(ctx));
-    CK(cudaMemcpyAsync(ctx->red_host + 2, ctx->red + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(ctx->red_host + 2, ctx->red_base + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     double nrm;
@@ -1390,6 +1091,7 @@ int prs_set_initial(prs_ctx *ctx, const double *u0, int u0_on_device) {
     ctx->u0norm = (nrm > 0.0) ? nrm : 1.0;
     ctx->have_initial = true;
     ctx->have_coarse = false;
+    ctx->gb_valid = false;
     return PRS_OK;
 }
 
@@ -1409,8 +1111,7 @@ int prs_coarse_sweep(prs_ctx *ctx) {
     if (!ctx) return PRS_EINVAL;
     if (!ctx->have_initial) { ctx->err = "prs_set_initial first"; return PRS_EINVAL; }
     TRY(ensure_factors(ctx, 0, ctx->dT));
-    if (ctx->nranks > 1 && ctx->rank > 0)
-        NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
+    if (ctx->nranks > 1 && ctx->rank > 0) NK(ctx->tr->recv(ctx->traj, (size_t)ctx->vol, ctx->rank - 1, ctx->stream));
     if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, 0, EPI_INIT));
     for (int i = sweep2_ok(ctx) ? ctx->count : 0; i < ctx->count; ++i) {
         EpiArgs ep;
@@ -1421,9 +1122,9 @@ int prs_coarse_sweep(prs_ctx *ctx) {
                      coarse_time(ctx, ctx->first + i), ep, false, ctx->ss));
     }
     if (ctx->nranks > 1 && ctx->rank < ctx->nranks - 1)
-        NK(g_nccl.Send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ncclDouble, ctx->rank + 1, ctx->comm,
-                       ctx->stream));
+        NK(ctx->tr->send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ctx->rank + 1, ctx->stream));
     ctx->have_coarse = true;
+    ctx->gb_valid = false;
     return PRS_OK;
 }
 
@@ -1436,7 +1137,7 @@ static int local_start(const prs_ctx *ctx) {
 // small 2-D slices (kappa = 1, n = 32 / 64 / 128 / 256): the whole sweep on chip (sweep2.cuh)
 static bool sweep2_ok(const prs_ctx *ctx) {
     const int n = ctx->p.n;
-    return !ctx->no_sweep2 && !ctx->force_v2 && ctx->p.dim == 2 && ctx->p.split == 0 && ctx->p.coef_kind == 0 &&
+    return !ctx->no_sweep2 && ctx->p.dim == 2 && ctx->p.split == 0 && ctx->p.coef_kind == 0 &&
            (n == 32 || n == 64 || n == 128 || n == 256);
 }
 
@@ -1589,10 +1290,17 @@ static int enqueue_fine_sweep(prs_ctx *ctx) {
 // of its captured CUDA graph.  Kernel arguments are the context's fixed buffers, so one
 // capture serves every later call.
 static int run_graphed(prs_ctx *ctx, int (*enqueue)(prs_ctx *), int &calls, cudaGraphExec_t &exec,
-                       long long &per_replay) {
+                       long long &per_replay, int &gen) {
     // (graphs are captured for the full batch: a converged prefix launches directly)
     const bool use = ctx->graphs && ctx->nranks == 1 && !ctx->prof && local_start(ctx) == 0;
     if (!use || calls++ == 0) return enqueue(ctx);
+    if (exec && gen != ctx->scratch_gen + ctx->dd.gen) {
+        // scratch reallocated since the capture: the graph is stale; this call launches
+        // directly (sizing the scratch again), the next one captures anew
+        CK(cudaGraphExecDestroy(exec));
+        exec = nullptr;
+        return enqueue(ctx);
+    }
     if (!exec) {
         const long long l0 = ctx->launches;
         cudaGraph_t g = nullptr;
@@ -1616,6 +1324,7 @@ static int run_graphed(prs_ctx *ctx, int (*enqueue)(prs_ctx *), int &calls, cuda
         }
         per_replay = ctx->launches - l0;
         ctx->launches = l0;
+        gen = ctx->scratch_gen + ctx->dd.gen;
     }
     CK(cudaGraphLaunch(exec, ctx->stream));
     ctx->launches += per_replay;
@@ -1626,7 +1335,7 @@ int prs_fine_sweep(prs_ctx *ctx) {
     if (!ctx) return PRS_EINVAL;
     if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
     TRY(ensure_factors(ctx, 1, ctx->dt));
-    TRY(run_graphed(ctx, enqueue_fine_sweep, ctx->fine_calls, ctx->fine_exec, ctx->fine_glaunch));
+    TRY(run_graphed(ctx, enqueue_fine_sweep, ctx->fine_calls, ctx->fine_exec, ctx->fine_glaunch, ctx->fine_gen));
     ctx->delta = (ctx->p.s & 1) ? ctx->fa : ctx->fb;
     if (ctx->prof) TRY(prof_flush(ctx));
     return PRS_OK;
@@ -1691,14 +1400,10 @@ static int gp_phase1(prs_ctx *ctx, int b, const double *in, double *v, int slice
     x.s2f = ctx->s2f;
     const int coef = ctx->p.coef_kind, src = ctx->p.source_kind;
     void (*kx)(X3Args) = nullptr;
-    if (ctx->x3_tma) {
-        TRY(get_tmap(ctx, in, x.vol / LCH, &x.tm_in));
-        if (coef) TRY(get_tmap(ctx, f.invdx, (long long)n * n / LCH, &x.tm_piv));
-    }
-#define XK(C, S_) if (coef == C && src == S_) kx = ctx->x3_tma ? xpass3_kernel<C, 0, S_, 1> : xpass3_kernel<C, 0, S_, 0>;
+#define XK(C, S_) if (coef == C && src == S_) kx = xpass3_kernel<C, 0, S_>;
     XK(0, 0) XK(0, 1) XK(1, 0) XK(1, 1)
 #undef XK
-    const size_t shm = xpass3_smem_bytes(coef, ctx->x3_tma ? 1 : 0);
+    const size_t shm = xpass3_smem_bytes(coef);
     CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     kx<<<(unsigned)std::min<long long>(ctx->num_sms, x.ngroups), X3T, shm, ctx->stream>>>(x);
     TRY(last_launch(ctx));
@@ -1742,7 +1447,10 @@ static int gp_phase2(prs_ctx *ctx, int b, double *v, double *traj_next, double *
 //   phase 0 (scatter): band p of Delta_sl from owner(sl) to rank p;
 //   phase 1 (gather) : band p of U_{sl+1} to owner(sl) (its end state) and, at a rank edge, to
 //                      owner(sl+1) (its incoming state, local index 0); band p of Gcache_sl to
-//                      owner(sl).
+//                      owner(sl);
+//   phase 2 (seed)   : band p of U_{sl+1} from owner(sl) to rank p (what = 1): the bands of the
+//                      current iterate, before the first band chain after the trajectory was
+//                      written elsewhere (the chain's update norm compares against them).
 static int gpar_plan(int N, int nranks, int me, int phase, std::vector<int> &ops) {
     ops.clear();
     const int P = nranks;
@@ -1756,13 +1464,14 @@ static int gpar_plan(int N, int nranks, int me, int phase, std::vector<int> &ops
     auto push = [&](int kind, int what, int sl, int band, int peer, int lidx) {
         ops.insert(ops.end(), {kind, what, sl, band, peer, lidx});
     };
-    if (phase == 0) {
+    if (phase == 0 || phase == 2) {
+        const int what = (phase == 0) ? 0 : 1, off = (phase == 0) ? 0 : 1;
         for (int sl = 0; sl < N; ++sl) {
             const int q = own[sl];
             if (q == me) {
-                for (int p = 0; p < P; ++p) push(p == me ? 2 : 0, 0, sl, p, p, sl - first[q]);
+                for (int p = 0; p < P; ++p) push(p == me ? 2 : 0, what, sl, p, p, sl + off - first[q]);
             } else {
-                push(1, 0, sl, me, q, -1);
+                push(1, what, sl, me, q, -1);
             }
         }
         return PRS_OK;
@@ -1808,34 +1517,39 @@ static int gp_correct(prs_ctx *ctx) {
     const int me = ctx->rank, N = ctx->p.N;
     // U_0's band (U^{k+1}_0 = U_0)
     CK(cudaMemcpyAsync(ctx->gb_u, ctx->u0 + (long long)me * bvol, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
-    // scatter: band p of Delta_n from owner(n) to rank p
+    // phase 2 (seed, when stale): band p of U^k_{n+1} from owner(n) to rank p;
+    // phase 0 (scatter): band p of Delta_n from owner(n) to rank p
     std::vector<int> ops;
-    TRY(gpar_plan(N, ctx->nranks, me, 0, ops));
-    NK(g_nccl.GroupStart());
-    for (size_t o = 0; o < ops.size(); o += 6) {
-        const int kind = ops[o], sl = ops[o + 2], band = ops[o + 3], peer = ops[o + 4], lidx = ops[o + 5];
-        if (kind == 1) {
-            NK(g_nccl.Recv(ctx->gb_d + sl * bvol, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
-        } else {
-            const double *d = state(ctx, ctx->delta, lidx) + band * bvol;
-            if (kind == 2)
-                CK(cudaMemcpyAsync(ctx->gb_d + sl * bvol, d, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
-            else
-                NK(g_nccl.Send(d, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
+    for (int phase : {2, 0}) {
+        if (phase == 2 && ctx->gb_valid) continue;
+        TRY(gpar_plan(N, ctx->nranks, me, phase, ops));
+        double *mine = (phase == 0) ? ctx->gb_d : ctx->gb_u + bvol;  // band of slice sl at + sl * bvol
+        const double *src = (phase == 0) ? ctx->delta : ctx->traj;
+        NK(ctx->tr->group_start());
+        for (size_t o = 0; o < ops.size(); o += 6) {
+            const int kind = ops[o], sl = ops[o + 2], band = ops[o + 3], peer = ops[o + 4], lidx = ops[o + 5];
+            if (kind == 1) {
+                NK(ctx->tr->recv(mine + sl * bvol, (size_t)bvol, peer, ctx->stream));
+            } else {
+                const double *d = state(ctx, const_cast<double *>(src), lidx) + band * bvol;
+                if (kind == 2)
+                    CK(cudaMemcpyAsync(mine + sl * bvol, d, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+                else
+                    NK(ctx->tr->send(d, (size_t)bvol, peer, ctx->stream));
+            }
         }
+        NK(ctx->tr->group_end());
     }
-    NK(g_nccl.GroupEnd());
     // the chain on this rank's band: exchange the band tuples after phase 1 of every step
     for (int sl = 0; sl < N; ++sl) {
         TRY(gp_phase1(ctx, me, ctx->gb_u + sl * bvol, ctx->gb_v, sl));
-        NK(g_nccl.AllGather(ctx->gb_tot + (long long)me * 5 * n, ctx->gb_tot, (size_t)5 * n, ncclDouble, ctx->comm,
-                            ctx->stream));
+        NK(ctx->tr->allgather_inplace(ctx->gb_tot, (size_t)5 * n, ctx->stream));
         TRY(gp_phase2(ctx, me, ctx->gb_v, ctx->gb_u + (sl + 1) * bvol, ctx->gb_gc + sl * bvol,
                       ctx->gb_d + sl * bvol));
     }
     // gather: U_{n+1} and Gcache_n bands to the owner of slice n, and U_first to this rank
     TRY(gpar_plan(N, ctx->nranks, me, 1, ops));
-    NK(g_nccl.GroupStart());
+    NK(ctx->tr->group_start());
     for (size_t o = 0; o < ops.size(); o += 6) {
         const int kind = ops[o], what = ops[o + 1], sl = ops[o + 2], band = ops[o + 3], peer = ops[o + 4],
                   lidx = ops[o + 5];
@@ -1844,11 +1558,12 @@ static int gp_correct(prs_ctx *ctx) {
         if (kind == 2)
             CK(cudaMemcpyAsync(dst, mine, bbytes, cudaMemcpyDeviceToDevice, ctx->stream));
         else if (kind == 0)
-            NK(g_nccl.Send(mine, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
+            NK(ctx->tr->send(mine, (size_t)bvol, peer, ctx->stream));
         else
-            NK(g_nccl.Recv(dst, (size_t)bvol, ncclDouble, peer, ctx->comm, ctx->stream));
+            NK(ctx->tr->recv(dst, (size_t)bvol, peer, ctx->stream));
     }
-    NK(g_nccl.GroupEnd());
+    NK(ctx->tr->group_end());
+    ctx->gb_valid = true;  // gb_u[1..N] = this rank's bands of U^{k+1}, as gathered into traj
     return PRS_OK;
 }
 
@@ -1869,46 +1584,119 @@ static int enqueue_correct_chain(prs_ctx *ctx) {
     return PRS_OK;
 }
 
-int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
-    if (!ctx) return PRS_EINVAL;
-    if (!ctx->delta) { ctx->err = "prs_fine_sweep first"; return PRS_EINVAL; }
-    if (ctx->gpar) {
-        TRY(gp_correct(ctx));
-        if (ctx->nranks > 1)
-            NK(g_nccl.AllReduce(ctx->red, ctx->red, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
-    } else if (ctx->nranks > 1) {
-        CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
-        if (ctx->rank > 0)
-            NK(g_nccl.Recv(ctx->traj, (size_t)ctx->vol, ncclDouble, ctx->rank - 1, ctx->comm, ctx->stream));
-        if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, local_start(ctx), EPI_CORRECT));
-        for (int i = sweep2_ok(ctx) ? ctx->count : local_start(ctx); i < ctx->count; ++i) {
-            EpiArgs ep;
-            ep.kind = EPI_CORRECT;
-            ep.gcache = state(ctx, ctx->gcache, i);
-            ep.delta = state(ctx, ctx->delta, i);
-            ep.traj = state(ctx, ctx->traj, i + 1);
-            TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
-                         coarse_time(ctx, ctx->first + i), ep, false, ctx->ss));
-        }
-        if (ctx->rank < ctx->nranks - 1)
-            NK(g_nccl.Send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ncclDouble, ctx->rank + 1,
-                           ctx->comm, ctx->stream));
-        NK(g_nccl.AllReduce(ctx->red, ctx->red, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
-    } else {
-        TRY(run_graphed(ctx, enqueue_correct_chain, ctx->corr_calls, ctx->corr_exec, ctx->corr_glaunch));
+// The multi-rank coarse chain of one iteration on the context stream (owner-G: receive
+// U^{k+1}_first from the previous rank, G steps with the fused correction over the local slices,
+// send U^{k+1}_last on; space-parallel G: the band chain of gp_correct); the update / flag
+// maxima land in ctx->red (this rank's part).
+static int enqueue_chain_mr(prs_ctx *ctx) {
+    if (ctx->gpar) return gp_correct(ctx);
+    CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
+    if (ctx->rank > 0) NK(ctx->tr->recv(ctx->traj, (size_t)ctx->vol, ctx->rank - 1, ctx->stream));
+    if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, local_start(ctx), EPI_CORRECT));
+    for (int i = sweep2_ok(ctx) ? ctx->count : local_start(ctx); i < ctx->count; ++i) {
+        EpiArgs ep;
+        ep.kind = EPI_CORRECT;
+        ep.gcache = state(ctx, ctx->gcache, i);
+        ep.delta = state(ctx, ctx->delta, i);
+        ep.traj = state(ctx, ctx->traj, i + 1);
+        TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1,
+                     coarse_time(ctx, ctx->first + i), ep, false, ctx->ss));
     }
-    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->rank < ctx->nranks - 1)
+        NK(ctx->tr->send(state(ctx, ctx->traj, ctx->count), (size_t)ctx->vol, ctx->rank + 1, ctx->stream));
+    return PRS_OK;
+}
+
+// (update, flag) pair at host `h` -> normalised update; PRS_EDIVERGED on a non-finite value
+static int read_update(prs_ctx *ctx, const unsigned long long *h, double *update_out) {
     double upd;
-    memcpy(&upd, ctx->red_host, sizeof(double));
+    memcpy(&upd, h, sizeof(double));
     if (update_out) *update_out = upd / ctx->u0norm;
-    ctx->delta = nullptr;
-    if (ctx->red_host[1]) {
+    if (h[1]) {
         ctx->err = "non-finite value in the parareal iterate";
         return PRS_EDIVERGED;
     }
     return PRS_OK;
+}
+
+int prs_parareal_correct(prs_ctx *ctx, double *update_out) {
+    if (!ctx) return PRS_EINVAL;
+    if (!ctx->delta) { ctx->err = "prs_fine_sweep first"; return PRS_EINVAL; }
+    if (ctx->nranks > 1) {
+        TRY(enqueue_chain_mr(ctx));
+        NK(ctx->tr->allreduce_max_u64(ctx->red, 2, ctx->stream, 1));
+    } else if (ctx->gpar) {
+        TRY(gp_correct(ctx));
+    } else {
+        TRY(run_graphed(ctx, enqueue_correct_chain, ctx->corr_calls, ctx->corr_exec, ctx->corr_glaunch, ctx->corr_gen));
+    }
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->delta = nullptr;
+    return read_update(ctx, ctx->red_host, update_out);
+}
+
+// prs_iterate over several ranks with a lagged stop test:
+// the stop-test all-reduce of iteration k runs on its own stream (and NCCL communicator) once
+// this rank's chain of k is done, while the context stream already runs the fine sweep of
+// iteration k + 1 (it needs only U^{k+1}_n); the host reads iteration k's
+// update while that sweep runs.  On a stop, the lookahead sweep has written only the Delta
+// scratch: trajectory, k and update history are those of the unlagged loop.  The (update,
+// flag) words alternate between two parities so chain k + 1 never clears the pair the
+// all-reduce of k still reads.
+static int iterate_lagged(prs_ctx *ctx, int K, double tol, int *k_out, double *hist) {
+    if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
+    if (!ctx->ctl) {
+        CK(cudaStreamCreateWithFlags(&ctx->ctl, cudaStreamNonBlocking));
+        for (int p = 0; p < 2; ++p) {
+            CK(cudaEventCreateWithFlags(&ctx->ev_chain[p], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_red[p], cudaEventDisableTiming | cudaEventBlockingSync));
+        }
+    }
+    TRY(ensure_factors(ctx, 0, ctx->dT));
+    TRY(ensure_factors(ctx, 1, ctx->dt));
+    int k = 0, rc = PRS_OK;
+    ctx->kconv = 0;
+    if (K > 0) {
+        rc = enqueue_fine_sweep(ctx);
+        ctx->delta = (ctx->p.s & 1) ? ctx->fa : ctx->fb;
+    }
+    while (rc == PRS_OK && k < K) {
+        const int p = k & 1;
+        ctx->red = ctx->red_base + 4 * p;
+        rc = enqueue_chain_mr(ctx);
+        if (rc != PRS_OK) break;
+        CK(cudaEventRecord(ctx->ev_chain[p], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->ctl, ctx->ev_chain[p], 0));
+        rc = ctx->tr->allreduce_max_u64(ctx->red, 2, ctx->ctl, 1);
+        if (rc != PRS_OK) {
+            ctx->err = ctx->tr->err;
+            break;
+        }
+        CK(cudaMemcpyAsync(ctx->red_host + 4 * p, ctx->red, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           ctx->ctl));
+        CK(cudaEventRecord(ctx->ev_red[p], ctx->ctl));
+        if (k + 1 < K) {  // lookahead: iteration k+1's fine sweep (slices n < k+1 converged)
+            ctx->kconv = ctx->skip_converged ? k + 1 : 0;
+            rc = enqueue_fine_sweep(ctx);
+            if (rc != PRS_OK) break;
+        }
+        CK(cudaEventSynchronize(ctx->ev_red[p]));
+        double upd = 0.0;
+        rc = read_update(ctx, ctx->red_host + 4 * p, &upd);
+        if (hist) hist[k] = upd;
+        ++k;
+        if (rc != PRS_OK || upd <= tol) break;
+    }
+    // drain (a lookahead sweep wrote only the Delta scratch)
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->ctl);
+    ctx->red = ctx->red_base;
+    ctx->kconv = 0;
+    ctx->delta = nullptr;
+    if (k_out) *k_out = k;
+    return rc;
 }
 
 // ---------------------------------------------------------- pipelined parareal -------
@@ -2027,6 +1815,7 @@ int prs_set_pipeline(prs_ctx *ctx, int blocks) {
 
 int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
     if (!ctx || kmax < 0) return PRS_EINVAL;
+    if (ctx->nranks > 1 && ctx->lag) return iterate_lagged(ctx, kmax < ctx->p.N ? kmax : ctx->p.N, tol, k_out, hist);
     if (ctx->pipe && !ctx->gpar) {  // (space-parallel G takes the unpipelined chain)
         if (!ctx->have_coarse) { ctx->err = "prs_coarse_sweep first"; return PRS_EINVAL; }
         return pipe_iterate(ctx, kmax < ctx->p.N ? kmax : ctx->p.N, tol, k_out, hist);
@@ -2128,7 +1917,7 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
 }
 
 int prs_gpar_plan(int N, int nranks, int rank, int phase, int *ops, int max_ops) {
-    if (N < 1 || nranks < 1 || rank < 0 || rank >= nranks || (phase != 0 && phase != 1) || max_ops < 0) return -1;
+    if (N < 1 || nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2 || max_ops < 0) return -1;
     std::vector<int> v;
     if (gpar_plan(N, nranks, rank, phase, v) != PRS_OK) return -1;
     const int cnt = (int)(v.size() / 6);
@@ -2159,6 +1948,7 @@ int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands) {
     }
     ctx->gP = P;
     ctx->gnb = n / P;
+    ctx->gb_valid = false;
     const long long bvol = (long long)ctx->gnb * n, nrb = ctx->gnb / L5RB;
     double **bufs[] = {&ctx->gb_u, &ctx->gb_d, &ctx->gb_gc, &ctx->gb_v, &ctx->gb_tt, &ctx->gb_tot, &ctx->gb_yx};
     for (double **b : bufs)

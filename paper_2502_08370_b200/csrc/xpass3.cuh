@@ -14,8 +14,6 @@
 // DR's neighbour rows come from the same ring (row j-1 / j+1 of the previous / next group),
 // so every state row is read from HBM once per pass.
 #pragma once
-#include <cuda.h>
-
 #include "common.cuh"
 
 namespace prs {
@@ -25,8 +23,6 @@ constexpr int X3C = 18;         // shared stride of a chunk (16 + 2 pad, 16-byte
 constexpr int X3G = X3T * X3C;  // doubles per group buffer
 
 struct X3Args {
-    CUtensorMap tm_in;    // TMA: the input batch as rows of 16 doubles (128-byte swizzle), box 16 x 256
-    CUtensorMap tm_piv;   // TMA: the x pivots (variable kappa) likewise
     const double *in;
     double *out;
     long long vol;        // points per state
@@ -51,8 +47,7 @@ struct X3Args {
     const double *invd, *s2n, *s2f;
 };
 
-inline size_t xpass3_smem_bytes(int coef, int tma = 0) {
-    if (tma) return sizeof(double) * ((size_t)(4 + (coef ? 2 : 1)) * X3T * LCH) + 1024 + sizeof(double2) * 16;
+inline size_t xpass3_smem_bytes(int coef) {
     return sizeof(double) * ((size_t)(4 + (coef ? 2 : 1)) * X3G) + sizeof(double2) * 16;
 }
 
@@ -66,29 +61,15 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// TMA = 1: every group (4096 doubles = 256 rows of 128 bytes) arrives as ONE 2-D tensor copy
-// issued by one thread, completing on the slot's mbarrier; the tensor map's 128-byte swizzle
-// puts 16-byte unit u of thread k's chunk (row k) at unit u ^ (k & 7), so the per-thread chunk
-// reads stay bank-conflict free without padding.  TMA = 0: 8 16-byte cp.async per thread per
-// group into the padded (stride-18) chunk layout.
-template <int COEF, int DR, int SRC, int TMA>
+// Group copies: 8 16-byte cp.async per thread per group into the padded (stride-18) chunk
+// layout.  (A TMA tensor-copy ring was measured ~3 % slower on c3: the pass is bound by its
+// row latency chain, not by the copy issue.)
+template <int COEF, int DR, int SRC>
 __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ X3Args a) {
-    extern __shared__ __align__(16) double smem_raw[];
-    // TMA: slots 1024-byte aligned (swizzle atom), unpadded
-    double *smem = TMA ? reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023)
-                       : smem_raw;
-    constexpr int SLOT = TMA ? X3T * LCH : X3G;  // doubles per ring slot
-    __shared__ __align__(8) unsigned long long mbu[4], mbp[2];  // TMA: per ring slot
-    if (TMA && threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(mbu + i, 1);
-        for (int i = 0; i < 2; ++i) mbar_init(mbp + i, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    unsigned npu = 0, npp = 0;       // TMA: parity the next fill of each slot will complete (bits)
-    unsigned filledu = 0, filledp = 0;
+    extern __shared__ __align__(16) double smem[];
+    constexpr int SLOT = X3G;  // doubles per ring slot
     // offset (doubles) of 16-byte unit u of chunk (row) r within a slot
-    auto uoff = [&](int r, int u) { return TMA ? r * LCH + ((u ^ (r & 7)) << 1) : r * X3C + 2 * u; };
+    auto uoff = [&](int r, int u) { return r * X3C + 2 * u; };
     double *ubuf = smem;                          // 4 slots: ring of state groups
     double *ibuf = smem + 4 * SLOT;               // COEF: 2 pivot slots; else 1 out staging slot
     double2 *scr = reinterpret_cast<double2 *>(smem + (4 + (COEF ? 2 : 1)) * SLOT);
@@ -137,30 +118,8 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ 
     }
     __syncthreads();  // the previous range's buffers are free
 
-    // issue the copies of group g into a slot: TMA (one thread, one tensor copy; `trow` = the
-    // tensor row of the group's first 128-byte row) or cp.async (all threads)
-    auto issue_group = [&](const double *src, long long g, double *dst, const CUtensorMap *tm, long long trow) {
-        if (TMA) {
-            const int slot = (int)((dst - ubuf) / SLOT);  // state ring 0..3, pivot ring 4..5
-            unsigned long long *mb = (slot < 4) ? mbu + slot : mbp + (slot - 4);
-            if (slot < 4) {
-                npu ^= 1u << slot;
-                filledu |= 1u << slot;
-            } else {
-                npp ^= 1u << (slot - 4);
-                filledp |= 1u << (slot - 4);
-            }
-            if (k == 0) {
-                mbar_arrive_expect(mb, (unsigned)(group_elems * sizeof(double)));
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-                    "[%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                    "l"(reinterpret_cast<unsigned long long>(tm)), "r"(0), "r"((int)trow),
-                    "r"((unsigned)__cvta_generic_to_shared(mb))
-                    : "memory");
-            }
-            return;
-        }
+    // issue the copies of group g into a slot (all threads)
+    auto issue_group = [&](const double *src, long long g, double *dst) {
         const double *s = src + g * group_elems;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -169,26 +128,17 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ 
             cp_async16(dst + c * X3C + 2 * u, s + 2 * p);
         }
     };
-    // TMA: wait until the most recent fill of a slot has landed (parity of that fill)
-    auto wait_u = [&](long long g) {
-        const int sl = (int)(g & 3);
-        if (TMA && ((filledu >> sl) & 1)) mbar_wait(mbu + sl, ((npu >> sl) & 1) ^ 1);
-    };
-    auto wait_p = [&](long long g) {
-        const int sl = COEF ? (int)(g & 1) : 0;
-        if (TMA && COEF && ((filledp >> sl) & 1)) mbar_wait(mbp + sl, ((npp >> sl) & 1) ^ 1);
-    };
     // state groups are contiguous in memory across the whole batch: group g = elements
     // [g*4096, (g+1)*4096) of the batch buffer; a group never splits a line (n | 4096).
     const double *pin = a.in;
     auto ub = [&](long long g) { return ubuf + (int)(g & 3) * SLOT; };
     auto ib = [&](long long g) { return ibuf + (COEF ? (int)(g & 1) : 0) * SLOT; };
-    auto issue_state = [&](long long g) { issue_group(pin, g, ub(g), &a.tm_in, g * (group_elems / LCH)); };
+    auto issue_state = [&](long long g) { issue_group(pin, g, ub(g)); };
     // pivot rows repeat every state: the group of pivots for global group g starts at
     // row (g * lpg) mod lines_per_state
     auto issue_piv = [&](long long g) {
         const long long row0 = ((g * lpg) & (a.lines_per_state - 1)) + a.row0;
-        issue_group(a.invd + row0 * n - 0, 0, ib(g), &a.tm_piv, row0 * n / LCH);
+        issue_group(a.invd + row0 * n, 0, ib(g));
     };
 
     // prologue: U(g0-1) (DR halo), U(g0), U(g0+1), pivots(g0)
@@ -235,15 +185,8 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ 
         // prefetch two ahead (state) / one ahead (pivots)
         if (g + 2 < G && g + 2 < g1 + (DR ? 1 : 0)) issue_state(g + 2);
         if (COEF && g + 1 < g1) issue_piv(g + 1);
-        if (TMA) {
-            if (DR && g > 0) wait_u(g - 1);
-            wait_u(g);
-            if (DR && g + 1 < G) wait_u(g + 1);
-            if (COEF) wait_p(g);
-        } else {
-            cp_async_commit();
-            cp_async_wait<1>();
-        }
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
 
         // line of this thread: global line index, state, row
@@ -373,20 +316,9 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ 
                 *reinterpret_cast<double2 *>(o + 2 * p) = xx;
             }
         }
-        // the staging slot gets the next pivot group by TMA: order these generic accesses
-        // before the async proxy's writes
-        if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();  // staging buffer free before the next prefetch lands in it
     }
-    if (TMA) {  // every fill issued in this range has landed before the slots are reused
-        for (int sl = 0; sl < 4; ++sl)
-            if ((filledu >> sl) & 1) mbar_wait(mbu + sl, ((npu >> sl) & 1) ^ 1);
-        if (COEF)
-            for (int sl = 0; sl < 2; ++sl)
-                if ((filledp >> sl) & 1) mbar_wait(mbp + sl, ((npp >> sl) & 1) ^ 1);
-    } else {
-        cp_async_wait<0>();
-    }
+    cp_async_wait<0>();
     }  // tasks
 }
 

@@ -140,3 +140,32 @@ def initial_state(prob: Problem) -> np.ndarray:
         rng = np.random.default_rng(prob.seed)
         return rng.standard_normal((n,) * prob.dim)
     raise ValueError(prob.init)
+
+
+# ------------------------------------------------------- digests of large trajectories
+# (used to compare runs whose full states are too large to store: a fixed seeded set of
+# sample points and +-1 random projections; pure index / sign generation, no method arithmetic)
+def sample_indices(npts: int, count: int = 128, seed: int = 2502) -> np.ndarray:
+    """`count` distinct flat indices into a state of npts points (first and last included)."""
+    rng = SplitMix64(seed)
+    picked = {0, npts - 1}
+    while len(picked) < min(count, npts):
+        picked.add(rng.below(npts))
+    return np.array(sorted(picked), dtype=np.int64)
+
+
+def projection_signs(npts: int, count: int = 4, seed: int = 8370) -> np.ndarray:
+    """count x npts matrix of +-1.0 (SplitMix64 bits)."""
+    rng = SplitMix64(seed)
+    out = np.empty((count, npts))
+    for r in range(count):
+        words = np.array([rng.next() for _ in range((npts + 63) // 64)], dtype=np.uint64)
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:npts]
+        out[r] = 1.0 - 2.0 * bits
+    return out
+
+
+def digest(states: np.ndarray, idx: np.ndarray, signs: np.ndarray) -> dict:
+    """Per state of `states` (S x npts): sampled values, projections, inf norm."""
+    flat = np.asarray(states, dtype=np.float64).reshape(states.shape[0], -1)
+    return {"samples": flat[:, idx], "proj": flat @ signs.T, "inf": np.max(np.abs(flat), axis=1)}

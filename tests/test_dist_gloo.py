@@ -181,10 +181,17 @@ def _gpar_plan_worker(rank, world, N, L):
     gb_d = torch.full((N, L), -1.0)
     gb_u = torch.stack([torch.full((L,), code(sl, rank, 2)) for sl in range(N + 1)])
     gb_gc = torch.stack([torch.full((L,), code(sl, rank, 3)) for sl in range(N)])
-    for phase in (0, 1):
+    # the owner's U^k end states (local index 1..count), tagged 4, for the seed phase
+    trajk = torch.stack([torch.stack([torch.full((L,), code(first + i, p, 4)) for p in range(P)])
+                         for i in range(count + 1)])
+    seeded = torch.full((N + 1, L), -1.0)
+    for phase in (2, 0, 1):
         reqs = []
         for kind, what, sl, band, peer, lidx in prs.gpar_plan(N, P, rank, phase):
-            if phase == 0:
+            if phase == 2:
+                assert what == 1
+                src, dst = (trajk[lidx, band] if kind != 1 else None), seeded[sl + 1]
+            elif phase == 0:
                 src, dst = (delta[lidx, band] if kind != 1 else None), gb_d[sl]
             else:
                 src = gb_u[sl + 1] if what == 1 else gb_gc[sl]
@@ -202,15 +209,16 @@ def _gpar_plan_worker(rank, world, N, L):
                 r[2].copy_(r[1])
             else:
                 r.wait()
-    return {"first": first, "count": count, "gb_d": gb_d[:, 0].tolist(),
+    return {"first": first, "count": count, "gb_d": gb_d[:, 0].tolist(), "seeded": seeded[:, 0].tolist(),
             "traj": traj[:, :, 0].tolist(), "gcache": gcache[:, :, 0].tolist()}
 
 
 @pytest.mark.parametrize("world,N", [(2, 8), (3, 7), (4, 8)])
 def test_space_parallel_g_exchange_plan(world, N):
-    """SURVEY 8(e) space-parallel G: Delta bands reach their band ranks and every owner gets
-    back all P bands of its U_{n+1}, its incoming U_first and its G cache (the exact op list
-    prs_parareal_correct issues to NCCL, run over gloo)."""
+    """SURVEY 8(e) space-parallel G: the seed phase gives every rank its band of the current
+    iterate U^k_1..U^k_N, Delta bands reach their band ranks and every owner gets back all P
+    bands of its U_{n+1}, its incoming U_first and its G cache (the exact op list
+    prs_parareal_correct issues to the transport, run over gloo)."""
     import paper_2502_08370_b200 as prs
     prs.build()  # no-op when libprs.so is current (host logic only: no GPU needed)
     prs.lib()
@@ -220,6 +228,8 @@ def test_space_parallel_g_exchange_plan(world, N):
         assert not isinstance(o, str), o
         first, count = o["first"], o["count"]
         assert o["gb_d"] == [1000.0 * sl + 10 * rank + 1 for sl in range(N)]
+        # seed: this rank's band of every U^k_{n+1}, n = 0..N-1, from the slice owners
+        assert o["seeded"][1:] == [1000.0 * (sl + 1) + 10 * rank + 4 for sl in range(N)]
         for i in range(1, count + 1):
             assert o["traj"][i] == [1000.0 * (first + i) + 10 * p + 2 for p in range(world)]
         if rank > 0:

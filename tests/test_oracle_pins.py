@@ -200,6 +200,19 @@ def test_partition_of_unity(ramp):
         assert vals == [(2 * k + 1) / 16 for k in range(7, -1, -1)]
     else:
         assert o.rho(0, w * 1 + 0.5) == pytest.approx(0.5, abs=1e-15)
+    # every node and face of every ramp against the ramp written out here: across interface m
+    # (face w m + 1/2) the colour of the strip on the left falls from 1 at x_l = w m + 1/2 - beta/2
+    # to 0 at x_l + beta, linearly (BASELINE c4) or as (1 + cos(pi u))/2,
+    # u = (x - x_l)/beta; it is colour 0 when the left strip is even (R6)
+    for m in range(1, S):
+        xl = w * m + 0.5 - ov / 2
+        for d2 in range(0, 2 * ov + 1):
+            x = xl + 0.5 * d2
+            u = (x - xl) / ov
+            down = (1.0 - u) if ramp == 0 else 0.5 * (1.0 + math.cos(math.pi * u))
+            want = down if (m - 1) % 2 == 0 else 1.0 - down
+            assert abs(o.rho(0, x) - want) <= 2e-16, (m, x)
+            assert abs(o.rho(1, x) - (1.0 - want)) <= 2e-16, (m, x)
 
 
 # -------------------------------------------------- P5 dense solves
@@ -460,13 +473,20 @@ def test_dd_fine_propagator_is_first_order():
 
 
 def test_determinism():
-    """P12: bitwise identical reruns."""
-    p = Problem(dim=2, n=12, N=4, s=3, G=FIE, F=DR, coef=1, init="random")
+    """P12: bitwise identical reruns, also with the per-slice F / G
+    evaluations of an iteration spread over threads (independent slices)."""
+    p = Problem(dim=2, n=12, N=5, s=3, G=FIE, F=DR, coef=1, init="random")
     o = oracle.Oracle(p)
     u0 = synth.initial_state(p)
-    a, _ = o.parareal(u0, 2, fixed=True)
-    b, _ = o.parareal(u0, 2, fixed=True)
+    a, _ = o.parareal(u0, 3, fixed=True)
+    b, _ = o.parareal(u0, 3, fixed=True)
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    try:
+        oracle.set_threads(4)
+        c, _ = o.parareal(u0, 3, fixed=True)
+    finally:
+        oracle.set_threads(1)
+    assert all(np.array_equal(x, y) for x, y in zip(a, c))
 
 
 def test_c1_paper_pairing_fie_dr_contracts_per_mode():
@@ -591,3 +611,30 @@ def test_full_tensor_dd_split(p):
         r = rng.standard_normal(A.shape[0])
         v = o.solve(j, 0.05, r).reshape(-1)
         assert np.max(np.abs(v - np.linalg.solve(B, r))) <= 1e-12 * np.max(np.abs(r))
+
+
+# ------------------------------------------- extended-precision bound of one step
+XPREC_CASES = [
+    Problem(dim=2, n=17, c=1.0, coef=0, source=1),
+    Problem(dim=2, n=33, c=1.0, coef=1),
+    Problem(dim=3, n=9, c=1.0, source=1),
+    Problem(dim=2, n=32, c=1.0, split=1, dd_strips=4, dd_overlap=4, dd_ramp=0, source=1),
+    Problem(dim=2, n=32, c=1.0, split=1, dd_strips=4, dd_overlap=4, dd_ramp=1),
+    Problem(dim=2, n=24, c=1.0, coef=1, split=1, dd_strips=8, dd_overlap=2),
+]
+
+
+@pytest.mark.parametrize("p", XPREC_CASES, ids=lambda p: p.label() + f"_k{p.coef}_r{p.dd_ramp}")
+def test_steps_within_rounding_of_extended_precision(p):
+    """Noisy inputs (white noise, the worst case for DR's explicit term): the oracle's FIE / DR
+    steps sit within 8 eps64 (|U_n| + |tau A U_n| + |tau F| + |U_{n+1}|) of the step evaluated in
+    80-bit extended precision from the paper's formulas (tests/xprec.py; PAPER.md:151-157,
+    165-171).  A relative coefficient error of 1e-9 anywhere in the operators would exceed it."""
+    from tests.xprec import XStep, err_in_eps
+    xs = XStep(p)
+    o = oracle.Oracle(p)
+    u = np.random.default_rng(3 + p.n).standard_normal((p.n,) * p.dim)
+    for sch in ((FIE, DR) if p.dim == 2 else (FIE,)):
+        for tau, t in ((1e-4, 0.3), (0.37, 0.74)):
+            ref, scale = xs.step(sch, tau, t, u)
+            assert err_in_eps(o.step(sch, tau, t, u), ref, scale) <= 8.0, (sch, tau)
