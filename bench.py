@@ -77,7 +77,8 @@ def updates_per_step(p) -> int:
 
 def workload_config(p, name, n_gpus):
     sch = {0: "FIE", 1: "DR"}
-    return {"workload": name, "grid": f"{p.n}^{p.dim}", "kappa": "1+0.5sin2pix sin2piy" if p.coef else "1",
+    kap = {0: "1", 1: "1+0.5sin2pix sin2piy", 2: "full tensor d11=d22=1/(2+cos3pix cos2piy), d12=1/4"}[p.coef]
+    return {"workload": name, "grid": f"{p.n}^{p.dim}", "kappa": kap,
             "split": "dd" if p.split else "dimensional", "pairing": f"{sch[p.G]}-{sch[p.F]}",
             "N": p.N, "s": p.s, "slices_per_gpu": p.N // n_gpus,
             "state_MiB": (p.n ** p.dim) * 8 / 2 ** 20,
@@ -168,6 +169,8 @@ def oracle_sample(p, reps: int = 1):
 def oracle_reps_for(p):
     # about 10 s of serial oracle work per sample
     per_pt = {2: 0.6e-6 if p.coef else 0.12e-6, 3: 0.15e-6}[p.dim]
+    if p.split:  # band elimination of the DD strip blocks (bandwidth ~ strip width)
+        per_pt = 2.5e-5
     return max(1, int(10.0 / (per_pt * p.n ** p.dim)))
 
 

@@ -39,6 +39,7 @@
 
 #include "../../include/prs.h"
 #include "common.cuh"
+#include "ddfull.cuh"
 #include "lpass.cuh"
 #include "xpass3.cuh"
 
@@ -884,7 +885,25 @@ struct DDData {
     double2 *gtot = nullptr;    // [gcap][2][DD_WMAX]
     int gen = 0;                // bumped when gbuf / gtot are reallocated (captured graphs hold them)
     long long gcap = 0;
+    // full diffusion tensor (coef_kind 2, ddfull.cuh): d tables and per (slot, colour) the
+    // block-Thomas factors E_l^T, P_l^{-1} of every block
+    bool full = false;
+    double h = 0;
+    double *dxf = nullptr, *dyf = nullptr;
+    double **d_ET[3][2] = {}, **d_PI[3][2] = {};
 };
+
+inline DFOp df_op(const DDData &d, int colour) {
+    DFOp o;
+    o.n = d.n;
+    o.h2inv = d.h2inv;
+    o.c = d.c;
+    o.rhon = d.rhon + colour * d.n;
+    o.rhof = d.rhof + colour * (d.n + 1);
+    o.dxf = d.dxf;
+    o.dyf = d.dyf;
+    return o;
+}
 
 // block extents from the index-space geometry (host; integers only, R6)
 inline void dd_blocks(int n, int S, int ov, int colour, std::vector<int> &i0, std::vector<int> &W) {
@@ -901,11 +920,12 @@ inline void dd_blocks(int n, int S, int ov, int colour, std::vector<int> &i0, st
 }
 
 inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cudaStream_t st, std::string &err) {
-    (void)h;
-    if (p.coef_kind != 0) {
-        err = "DD splitting on the GPU path supports kappa = 1 only";
+    if (p.coef_kind != 0 && p.coef_kind != 2) {
+        err = "DD splitting on the GPU path: kappa = 1 or the full tensor of section 5.2";
         return PRS_EUNSUPPORTED;
     }
+    d.full = p.coef_kind == 2;
+    d.h = h;
     d.n = p.n;
     d.S = p.dd_strips;
     d.ov = p.dd_overlap;
@@ -923,8 +943,8 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     for (int col = 0; col < 2; ++col) {
         dd_blocks(d.n, d.S, d.ov, col, d.bi0[col], d.bW[col]);
         for (int w : d.bW[col])
-            if (w > DD_WMAX) {
-                err = "DD block wider than " + std::to_string(DD_WMAX) + " columns";
+            if (w > (d.full ? DF_WMAX : DD_WMAX)) {
+                err = "DD block wider than " + std::to_string(d.full ? DF_WMAX : DD_WMAX) + " columns";
                 return PRS_EUNSUPPORTED;
             }
     }
@@ -935,6 +955,15 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
         return PRS_ECUDA;
     }
     dd_rho_tables<<<(d.n + 1 + 255) / 256, 256, 0, st>>>(d.n, d.S, d.ov, d.ramp, d.rhon, d.rhof);
+    if (d.full) {
+        const long long tot = (long long)d.n * (d.n + 1);
+        if (cudaMalloc(&d.dxf, sizeof(double) * tot) != cudaSuccess ||
+            cudaMalloc(&d.dyf, sizeof(double) * tot) != cudaSuccess) {
+            err = "cudaMalloc (full-tensor tables) failed";
+            return PRS_ECUDA;
+        }
+        df_tables<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d.n, h, d.dxf, d.dyf);
+    }
     for (int col = 0; col < 2; ++col) {
         const size_t nb = d.bi0[col].size();
         if (cudaMalloc(&d.d_bi0[col], sizeof(int) * nb) != cudaSuccess ||
@@ -958,11 +987,54 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     return PRS_OK;
 }
 
+// full tensor: block-Thomas factors of every block of both colours (one CTA per block)
+inline int df_factors(DDData &d, int slot, double tau, cudaStream_t st, std::string &err) {
+    for (int col = 0; col < 2; ++col) {
+        const size_t nb = d.bi0[col].size();
+        std::vector<double *> hE(nb), hP(nb);
+        int wmax = 0;
+        for (size_t k = 0; k < nb; ++k) {
+            const int W = d.bW[col][k];
+            wmax = std::max(wmax, W);
+            const size_t bytes = sizeof(double) * (size_t)d.n * W * W;
+            if (cudaMalloc(&hE[k], bytes) != cudaSuccess || cudaMalloc(&hP[k], bytes) != cudaSuccess) {
+                err = "cudaMalloc (full-tensor factors) failed";
+                return PRS_ECUDA;
+            }
+            d.store[slot].insert(d.store[slot].end(), {hE[k], hP[k]});
+        }
+        double **dE, **dP;
+        if (cudaMalloc(&dE, sizeof(double *) * nb) != cudaSuccess || cudaMalloc(&dP, sizeof(double *) * nb) != cudaSuccess) {
+            err = "cudaMalloc (full-tensor pointer tables) failed";
+            return PRS_ECUDA;
+        }
+        d.store[slot].insert(d.store[slot].end(), {(double *)dE, (double *)dP});
+        cudaMemcpyAsync(dE, hE.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(dP, hP.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+        d.d_ET[slot][col] = dE;
+        d.d_PI[slot][col] = dP;
+        const size_t fsm = df_factor_smem_bytes(wmax);
+        if (cudaFuncSetAttribute(df_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) !=
+            cudaSuccess) {
+            err = "cudaFuncSetAttribute(df_factor_kernel) failed";
+            return PRS_ECUDA;
+        }
+        df_factor_kernel<<<(unsigned)nb, DF_FTHREADS, fsm, st>>>(df_op(d, col), d.d_bi0[col], d.d_bW[col], tau, dE,
+                                                               dP);
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+        err = "full-tensor factorisation failed";
+        return PRS_ECUDA;
+    }
+    return PRS_OK;
+}
+
 inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::string &err) {
     if (d.tau[slot] == tau) return PRS_OK;
     for (double *p : d.store[slot]) cudaFree(p);
     d.store[slot].clear();
     d.tau[slot] = tau;
+    if (d.full) return df_factors(d, slot, tau, st, err);
     const size_t fsm = sizeof(double) * ((size_t)DD_WMAX * DD_WMAX + 2 * (DD_WMAX / 2 + 1)) +
                        sizeof(int) * 2 * (DD_WMAX / 2 + 1);
     if (cudaFuncSetAttribute(dd_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) !=
@@ -1020,7 +1092,7 @@ inline void dd_free(DDData &d) {
     }
     if (d.gbuf) cudaFree(d.gbuf);
     if (d.gtot) cudaFree(d.gtot);
-    double *bufs[] = {d.rhon, d.rhof, d.Z};
+    double *bufs[] = {d.rhon, d.rhof, d.Z, d.dxf, d.dyf};
     for (double *p : bufs)
         if (p) cudaFree(p);
     for (int c = 0; c < 2; ++c) {
@@ -1035,6 +1107,55 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
                    unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err, long long &launches,
                    double src_amp, int src) {
     const int n = d.n;
+    if (d.full) {
+        for (int stage = 0; stage < 2; ++stage) {
+            DFStageArgs a{};
+            a.U = in;
+            a.V = out;
+            a.vol = (long long)n * n;
+            a.n = n;
+            a.B = (int)B;
+            a.stage = stage;
+            a.nblk = (int)d.bi0[stage].size();
+            a.bi0 = d.d_bi0[stage];
+            a.bW = d.d_bW[stage];
+            a.ET = d.d_ET[slot][stage];
+            a.PI = d.d_PI[slot][stage];
+            a.tau = d.tau[slot];
+            a.c = d.c;
+            a.op_me = df_op(d, stage);
+            a.op_ot = df_op(d, 1 - stage);
+            a.src_amp = src_amp;
+            a.sinpi = d.sinpi;
+            a.ta = ta;
+            a.epi = epi;
+            a.e_gc = gc;
+            a.e_gcache = gcache;
+            a.e_delta = delta;
+            a.e_traj = traj;
+            a.e_red = red;
+            void (*kern)(DFStageArgs) = nullptr;
+            const int dr = scheme == PRS_DR;
+#define DK(D, S_) if (dr == D && src == S_) kern = df_stage_kernel<D, S_>;
+            DK(0, 0) DK(0, 1) DK(1, 0) DK(1, 1)
+#undef DK
+            if (prof && prs_internal_prof_begin(prof) != PRS_OK) return PRS_ECUDA;
+            kern<<<(unsigned)(B * a.nblk), DF_THREADS, 0, st>>>(a);
+            launches++;
+            const cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                err = std::string("df_stage_kernel: ") + cudaGetErrorString(e);
+                return PRS_ECUDA;
+            }
+            if (prof) {
+                // algorithmic fp64 flops: two dense W x W mat-vecs per block row and state
+                double flops = 0.0;
+                for (int w : d.bW[stage]) flops += (double)n * (4.0 * w * w + 20.0 * w);
+                if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
+            }
+        }
+        return PRS_OK;
+    }
     const int CL = (n + DD_RMAX - 1) / DD_RMAX;
     const size_t shm = dd_stage_smem_bytes();
     for (int stage = 0; stage < 2; ++stage) {

@@ -75,6 +75,10 @@ CONFIGS = {
     # c4: 2-D 1024^2 DD, 8 strips, 8-cell overlap, linear ramp, manufactured, N = 32, s = 64
     "c4": Problem(dim=2, n=1024, c=1.0, split=1, dd_strips=8, dd_overlap=8, dd_ramp=0,
                   source=1, N=32, s=64, G=FIE, F=FIE, init="phi"),
+    # c5: c4's DD recipe with the full diffusion tensor of PAPER.md:523-528
+    # (d11 = d22 = 1/(2 + cos 3pi x cos 2pi y), d12 = 1/4), the paper's Parareal/FIE-FIE
+    "c5": Problem(dim=2, n=1024, c=1.0, coef=2, split=1, dd_strips=8, dd_overlap=8, dd_ramp=0,
+                  source=1, N=32, s=64, G=FIE, F=FIE, init="phi"),
 }
 
 
