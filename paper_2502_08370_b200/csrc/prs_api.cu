@@ -830,11 +830,12 @@ static int validate(const prs_problem *p, std::string &err) {
         err = "schemes must be PRS_FIE or PRS_DR";
         return PRS_EINVAL;
     }
-    if (p->coef_kind == 2) {
-        err = "full diffusion tensor (coef_kind 2, PAPER.md:520-546, NEXT-3): CPU oracle only so far";
+    if (p->coef_kind == 2 && (p->split != 1 || p->dim != 2)) {
+        err = "the full diffusion tensor (coef_kind 2, PAPER.md:520-546) needs the 2-D DD split (mixed "
+              "derivatives: dimensional splitting does not apply, SPEC.md:128)";
         return PRS_EUNSUPPORTED;
     }
-    if (p->coef_kind != 0 && p->coef_kind != 1) { err = "coef_kind must be 0, 1 or 2"; return PRS_EINVAL; }
+    if (p->coef_kind < 0 || p->coef_kind > 2) { err = "coef_kind must be 0, 1 or 2"; return PRS_EINVAL; }
     if (p->source_kind != 0 && p->source_kind != 1) { err = "source_kind must be 0 or 1"; return PRS_EINVAL; }
     if (p->split != 0 && p->split != 1) { err = "split must be 0 or 1"; return PRS_EINVAL; }
     if (p->split == 1) {

@@ -946,3 +946,23 @@ def test_full_tensor_full_size_steps():
         want = o.step(sch, tau, tn, u)
         assert nerr(host(out), want, want, u) <= TOL, (sch, tau)
     ctx.close()
+
+
+def test_c_client_runs_parareal_through_the_abi(tmp_path):
+    """tests/c/abi_smoke.c -- plain C, host buffers, prs_create / set_initial / coarse_sweep /
+    iterate / get_slice -- matches the oracle's iterate at the k it stopped at."""
+    import subprocess
+    from tests.test_abi import build_c_smoke
+    exe = build_c_smoke(str(tmp_path))
+    out = str(tmp_path / "out.bin")
+    subprocess.check_call([exe, out])
+    raw = open(out, "rb").read()
+    k = int(np.frombuffer(raw[:4], dtype=np.int32)[0])
+    hist = np.frombuffer(raw[4:4 + 8 * k], dtype=np.float64)
+    uN = np.frombuffer(raw[4 + 8 * k:], dtype=np.float64).reshape(48, 48)
+    p = Problem(dim=2, n=48, c=1.0, coef=1, source=1, N=6, s=5, G=FIE, F=DR, init="phi")
+    trajs, upds = oracle.Oracle(p).parareal(synth.initial_state(p), p.N, tol=1e-9)
+    assert k == len(upds)
+    assert np.allclose(hist, upds, rtol=0, atol=TOL * max(1.0, max(upds)))
+    scale = max(float(np.max(np.abs(t))) for t in trajs)
+    assert float(np.max(np.abs(uN - trajs[-1][p.N]))) / scale <= TOL
