@@ -148,22 +148,83 @@ def ncu_traffic(name):
 
 
 # ------------------------------------------------------------------ CPU oracle ---
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    return sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count() or 1))
+
+
 def oracle_sample(p, reps: int = 1):
-    """Time the oracle as it stands on a bounded sample: fine steps of one slice."""
+    """Time the oracle as it stands on a bounded sample: `reps` fine steps of one slice, the
+    process pinned to one host core for the sample (as taskset -c <core>)."""
     import oracle
     o = oracle.Oracle(p)
     u = synth.initial_state(p)
     dt = p.T / (p.N * p.s)
-    t0 = time.perf_counter()
-    for j in range(reps):
-        u = o.step(p.F, dt, float(j + 1) * dt, u)
-    sec = time.perf_counter() - t0
+    cores = host_cores()
+    pin = cores[0]
+    if hasattr(os, "sched_setaffinity"):
+        os.sched_setaffinity(0, {pin})
+    try:
+        t0 = time.perf_counter()
+        for j in range(reps):
+            u = o.step(p.F, dt, float(j + 1) * dt, u)
+        sec = time.perf_counter() - t0
+    finally:
+        if hasattr(os, "sched_setaffinity"):
+            os.sched_setaffinity(0, set(cores))
     upd = reps * p.n ** p.dim
-    sched = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
-    return upd / sec, sec, {"kind": "oracle", "cores": 1,
-                            "host_cores_available": len(sched) if sched else os.cpu_count(),
+    return upd / sec, sec, {"kind": "oracle", "cores": 1, "taskset": f"core {pin}", "cpu_model": cpu_model(),
+                            "host_cores_available": len(cores),
                             "sample": f"{reps} fine {'DR' if p.F else 'FIE'} step(s) of one slice at "
                                       f"{p.n}^{p.dim} (serial C oracle, -O2, no FMA contraction)"}
+
+
+def oracle_sample_all_cores(p, reps: int = 1):
+    """The oracle's slice-parallel mode on every host core: one slice's `reps` fine steps per
+    core, all cores at once (the oracle's per-slice F evaluations are independent, PAPER.md:206-210;
+    ctypes releases the GIL).  Returns (aggregate updates/s, seconds, threads)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    o = oracle.Oracle(p)
+    u0 = synth.initial_state(p)
+    dt = p.T / (p.N * p.s)
+    th = min(len(host_cores()), 64)
+
+    def one(b):
+        u = u0 * (1.0 + b / th)
+        for j in range(reps):
+            u = o.step(p.F, dt, float(j + 1) * dt, u)
+        return 0
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(th) as ex:
+        list(ex.map(one, range(th)))
+    sec = time.perf_counter() - t0
+    return th * reps * p.n ** p.dim / sec, sec, th
+
+
+def oracle_ttt_extrapolated(p, k, rate_serial, rate_all, threads):
+    """Oracle parareal to k iterations, extrapolated from the measured update rates: the literal
+    algorithm does N coarse steps, then per iteration N s fine + 2 N coarse steps (G(U^k_n) is
+    recomputed, G(U^{k+1}_n) along the chain); the slice-parallel mode spreads the N s + N
+    independent steps over the threads, the chain of N coarse steps stays serial."""
+    pts = p.n ** p.dim
+    serial = pts * (p.N + k * (p.N * p.s + 2 * p.N)) / rate_serial
+    par_rounds = -(-p.N // max(1, threads))
+    allc = pts * (p.N + k * (par_rounds * (p.s + 1) + p.N)) / (rate_all / max(1, threads))
+    return {"serial_s": serial, "all_cores_s": allc, "iterations": k,
+            "how": "measured oracle update rates x the work of the literal algorithm (coarse steps "
+                   "counted at the fine-scheme rate)"}
 
 
 def oracle_reps_for(p):
@@ -376,9 +437,15 @@ def run_prs(args):
                               for k, v in stats.items() if v[0]}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sec, meta = oracle_sample(p, oracle_reps_for(p))
+        reps = oracle_reps_for(p)
+        v, sec, meta = oracle_sample(p, reps)
         meta.update({"value": v, "unit": UNIT, "seconds": sec})
+        va, seca, th = oracle_sample_all_cores(p, max(1, reps // 2))
+        meta["all_cores"] = {"value": va, "unit": UNIT, "cores": th, "seconds": seca,
+                             "sample": f"{max(1, reps // 2)} fine step(s) of one slice per core, {th} cores"}
         cpu = meta
+        if ttt is not None:
+            ttt["oracle_extrapolated"] = oracle_ttt_extrapolated(p, ttt["iterations"], v, va, th)
     ctx.close()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

@@ -110,8 +110,9 @@ int prs_parareal_correct(prs_ctx *ctx, double *update_out);
  * propagating; results are those of the unlagged loop. */
 int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist);
 
-/* Copy the current iterate U^k_n (n = 0..N) to host or device memory.  Only the rank that
- * owns U_n (slice n-1's end state, or n = first for the incoming state) may call it. */
+/* Copy the current iterate U^k_n (n = 0..N) to host or device memory.  Only a rank that holds
+ * U_n (as slice n-1's end state, or as the start state of its first slice) may call it
+ * (PRS_EINVAL elsewhere; see prs_set_ownership for cyclic ownership). */
 int prs_get_slice(prs_ctx *ctx, int n, double *out, int out_on_device);
 
 /* One FIE/DR step of size tau from a device state `in` to device `out` (in != out), the
@@ -146,6 +147,19 @@ int prs_fine_solve(prs_ctx *ctx, const double *u0, int u0_on_device, int nslices
  *   Supported for the 2-D dimensional split with G = FIE, P and n powers of two, n <= 4096,
  *   n % (64 P) == 0 (PRS_EUNSUPPORTED otherwise).  Results equal owner-G up to rounding. */
 int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands);
+
+/* Slice ownership across ranks ("up to N_c processors"):
+ * mode 0 (default): contiguous blocks, rank order = time order (prs_partition);
+ * mode 1: cyclic -- slice n on rank n mod P.  prs_iterate skips the converged slices n < k at
+ *   iteration k; with contiguous blocks the ranks holding the first blocks fall
+ *   idle while the last rank keeps its N/P slices every iteration, with cyclic ownership every
+ *   rank keeps ceil or floor((N-k)/P) active slices (balanced without moving any state), at the
+ *   price of N-1 hand-offs per coarse chain instead of P-1.  Results are bitwise those of
+ *   mode 0 and of one rank.  Owner-G coarse mode, unpipelined; call before prs_coarse_sweep
+ *   (reallocates the trajectory; the initial state is kept).  With cyclic ownership U_n lives on
+ *   ranks n mod P (as slice n's start) and (n-1) mod P (as slice n-1's end); prs_get_slice
+ *   accepts either.  One rank: a no-op. */
+int prs_set_ownership(prs_ctx *ctx, int mode);
 
 /* Pipelined parareal for prs_iterate: blocks > 0 cuts
  * the local slices into `blocks` blocks and runs each iteration as a per-block dependency

@@ -22,7 +22,7 @@ EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
            "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_set_pipeline", "prs_gpar_plan", "prs_set_profiling", "prs_launches", "prs_kernel_stats",
            "prs_last_error", "prs_destroy", "prs_local_world_create", "prs_local_world_destroy",
-           "prs_create_local"]
+           "prs_create_local", "prs_set_ownership"]
 
 
 class PrsError(RuntimeError):
@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
             "prs_local_world_create": ([I, ctypes.POINTER(V)], I),
             "prs_local_world_destroy": ([V], None),
             "prs_create_local": ([ctypes.POINTER(prs_problem), I, V, V, ctypes.POINTER(V)], I),
+            "prs_set_ownership": ([V, I], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -251,6 +252,21 @@ class Context:
         """0: owner-G chain; 1: space-parallel G over P row bands (P = nranks, or `bands`
         virtual bands on one rank)."""
         self._check(self.L.prs_set_coarse_mode(self.h, mode, bands))
+
+    def set_ownership(self, mode: int):
+        """0: contiguous slice blocks; 1: cyclic (slice n on rank n mod P), see include/prs.h."""
+        self._check(self.L.prs_set_ownership(self.h, mode))
+        self.cyclic = mode == 1 and self.nranks > 1
+        if self.cyclic:
+            self.first, self.count = self.rank, len(range(self.rank, self.prob.N, self.nranks))
+        else:
+            self.first, self.count = partition(self.prob.N, self.nranks, self.rank)
+
+    def slices(self):
+        """Global indices of this rank's slices."""
+        if getattr(self, "cyclic", False):
+            return list(range(self.rank, self.prob.N, self.nranks))
+        return list(range(self.first, self.first + self.count))
 
     def set_pipeline(self, blocks: int):
         """Pipelined parareal for iterate(): `blocks` slice blocks (0: off)."""

@@ -46,14 +46,16 @@ struct CoefTab {
     const double *m, *id, *cc;
 };
 
-// Source time of state b of a launch: t = ((slice0 + b) * tmul + toff) * tstep
-// (fine step j of slice n: ((n s + j + 1) delta t), coarse: ((n + 1) Delta T); R2)
+// Source time of state b of a launch: t = ((slice0 + b sstride) * tmul + toff) * tstep
+// (fine step j of slice n: ((n s + j + 1) delta t), coarse: ((n + 1) Delta T); R2;
+// sstride = P when a rank owns every P-th slice, cyclic ownership)
 struct TimeArgs {
-    long long slice0, tmul, toff;
-    double tstep;
+    long long slice0 = 0, tmul = 0, toff = 0;
+    double tstep = 0.0;
+    long long sstride = 1;
 };
 __device__ __forceinline__ double src_time(const TimeArgs &ta, long long b) {
-    return (double)((ta.slice0 + b) * ta.tmul + ta.toff) * ta.tstep;
+    return (double)((ta.slice0 + b * ta.sstride) * ta.tmul + ta.toff) * ta.tstep;
 }
 
 // Copy `len` doubles of a global table into chunk-padded shared memory (whole CTA).

@@ -134,6 +134,11 @@ struct TauFactors {
 struct prs_ctx {
     prs_problem p{};
     int rank = 0, nranks = 1, first = 0, count = 0;
+    // slice ownership (prs_set_ownership): 0 contiguous blocks (local slice i = global first + i;
+    // traj[i] / traj[i+1] = its start / end state), 1 cyclic (local slice i = global rank + i P;
+    // traj[i] = start, tend[i] = end state: consecutive slices live on consecutive ranks)
+    int cyclic = 0;
+    double *tend = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int device = 0;
@@ -800,6 +805,24 @@ int prs_internal_prof_end(prs_ctx *ctx, int kind, double bytes) { return prof_en
 
 static double *state(prs_ctx *ctx, double *base, long long i) { return base + i * ctx->ss; }
 
+// global index of local slice i; the rank owning global slice n; the end state of local slice i
+static long long gslice(const prs_ctx *ctx, long long i) {
+    return ctx->cyclic ? ctx->rank + i * ctx->nranks : ctx->first + i;
+}
+static int owner_of(const prs_ctx *ctx, int n) {
+    if (ctx->cyclic) return n % ctx->nranks;
+    for (int q = 0; q < ctx->nranks; ++q) {
+        int f = 0, c = 0;
+        prs_partition(ctx->p.N, ctx->nranks, q, &f, &c);
+        if (n >= f && n < f + c) return q;
+    }
+    return -1;
+}
+static double *end_state(prs_ctx *ctx, long long i) {
+    return ctx->cyclic ? state(ctx, ctx->tend, i) : state(ctx, ctx->traj, i + 1);
+}
+static long long slice_stride(const prs_ctx *ctx) { return ctx->cyclic ? ctx->nranks : 1; }
+
 // ==================================================================== C ABI =========
 extern "C" {
 
@@ -1043,7 +1066,7 @@ void prs_destroy(prs_ctx *ctx) {
 #endif
     delete ctx->tr;
     double *bufs[] = {ctx->traj, ctx->fa, ctx->fb, ctx->gcache, ctx->gtmp, ctx->u0,
-                      ctx->sinpi, ctx->s2n, ctx->s2f};
+                      ctx->sinpi, ctx->s2n, ctx->s2f, ctx->tend};
     for (double *b : bufs)
         if (b) cudaFree(b);
     for (auto &f : ctx->fac) {
@@ -1112,6 +1135,24 @@ int prs_coarse_sweep(prs_ctx *ctx) {
     if (!ctx) return PRS_EINVAL;
     if (!ctx->have_initial) { ctx->err = "prs_set_initial first"; return PRS_EINVAL; }
     TRY(ensure_factors(ctx, 0, ctx->dT));
+    if (ctx->cyclic) {
+        // slice n on rank n mod P: receive U^0_n from the previous slice's rank, one G step with
+        // the initial-guess epilogue, hand U^0_{n+1} to the next slice's rank
+        for (int i = 0; i < ctx->count; ++i) {
+            const int n = (int)gslice(ctx, i);
+            if (n > 0) NK(ctx->tr->recv(state(ctx, ctx->traj, i), (size_t)ctx->vol, owner_of(ctx, n - 1), ctx->stream));
+            EpiArgs ep;
+            ep.kind = EPI_INIT;
+            ep.gcache = state(ctx, ctx->gcache, i);
+            ep.traj = end_state(ctx, i);
+            TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1, coarse_time(ctx, n), ep,
+                         false, ctx->ss));
+            if (n + 1 < ctx->p.N)
+                NK(ctx->tr->send(end_state(ctx, i), (size_t)ctx->vol, owner_of(ctx, n + 1), ctx->stream));
+        }
+        ctx->have_coarse = true;
+        return PRS_OK;
+    }
     if (ctx->nranks > 1 && ctx->rank > 0) NK(ctx->tr->recv(ctx->traj, (size_t)ctx->vol, ctx->rank - 1, ctx->stream));
     if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, 0, EPI_INIT));
     for (int i = sweep2_ok(ctx) ? ctx->count : 0; i < ctx->count; ++i) {
@@ -1131,6 +1172,11 @@ int prs_coarse_sweep(prs_ctx *ctx) {
 
 // first local slice that still needs work (prs_iterate's converged prefix, else 0)
 static int local_start(const prs_ctx *ctx) {
+    if (ctx->cyclic) {  // local slices with rank + i P < kconv
+        const int k = ctx->kconv - ctx->rank;
+        const int i0 = k <= 0 ? 0 : (k + ctx->nranks - 1) / ctx->nranks;
+        return i0 > ctx->count ? ctx->count : i0;
+    }
     const int k = ctx->kconv - ctx->first;
     return k <= 0 ? 0 : (k > ctx->count ? ctx->count : k);
 }
@@ -1158,6 +1204,7 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
     a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
     a.sinpi = ctx->sinpi;
     a.slice0 = slice0;
+    a.sstride = slice_stride(ctx);
     a.dt = ctx->dt;
     a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
     const int dr = (ctx->p.F == PRS_DR) ? 1 : 0, src = ctx->p.source_kind, epi = gc ? EPI_DELTA : EPI_STORE;
@@ -1217,6 +1264,7 @@ static int launch_chain2x(prs_ctx *ctx, double *traj, double *gcache, const doub
     a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
     a.sinpi = ctx->sinpi;
     a.slice0 = ctx->first + i0;
+    a.sstride = 1;
     a.dt = ctx->dT;
     a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
     const int dr = (ctx->p.G == PRS_DR) ? 1 : 0, src = ctx->p.source_kind;
@@ -1266,13 +1314,14 @@ static int enqueue_fine_sweep(prs_ctx *ctx) {
     if (B <= 0) return PRS_OK;
     if (sweep2_ok(ctx))
         return launch_sweep2(ctx, state(ctx, ctx->traj, i0), state(ctx, (s & 1) ? ctx->fa : ctx->fb, i0),
-                             state(ctx, ctx->gcache, i0), B, ctx->first + i0, s);
+                             state(ctx, ctx->gcache, i0), B, gslice(ctx, i0), s);
     const double *src = state(ctx, ctx->traj, i0);
     double *bufs[2] = {state(ctx, ctx->fa, i0), state(ctx, ctx->fb, i0)};
     for (int j = 0; j < s; ++j) {
         double *dst = bufs[j & 1];
         TimeArgs ta;
-        ta.slice0 = ctx->first + i0;
+        ta.slice0 = gslice(ctx, i0);
+        ta.sstride = slice_stride(ctx);
         ta.tmul = s;
         ta.toff = j + 1;
         ta.tstep = ctx->dt;
@@ -1592,6 +1641,25 @@ static int enqueue_correct_chain(prs_ctx *ctx) {
 static int enqueue_chain_mr(prs_ctx *ctx) {
     if (ctx->gpar) return gp_correct(ctx);
     CK(cudaMemsetAsync(ctx->red, 0, sizeof(unsigned long long) * 2, ctx->stream));
+    if (ctx->cyclic) {
+        // slices in time order; the first active one (global kconv) starts from the converged,
+        // frozen U^k_kconv it holds, every later one receives U^{k+1}_n from the previous slice's rank
+        for (int i = local_start(ctx); i < ctx->count; ++i) {
+            const int n = (int)gslice(ctx, i);
+            if (n > ctx->kconv)
+                NK(ctx->tr->recv(state(ctx, ctx->traj, i), (size_t)ctx->vol, owner_of(ctx, n - 1), ctx->stream));
+            EpiArgs ep;
+            ep.kind = EPI_CORRECT;
+            ep.gcache = state(ctx, ctx->gcache, i);
+            ep.delta = state(ctx, ctx->delta, i);
+            ep.traj = end_state(ctx, i);
+            TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1, coarse_time(ctx, n), ep,
+                         false, ctx->ss));
+            if (n + 1 < ctx->p.N)
+                NK(ctx->tr->send(end_state(ctx, i), (size_t)ctx->vol, owner_of(ctx, n + 1), ctx->stream));
+        }
+        return PRS_OK;
+    }
     if (ctx->rank > 0) NK(ctx->tr->recv(ctx->traj, (size_t)ctx->vol, ctx->rank - 1, ctx->stream));
     if (sweep2_ok(ctx)) TRY(launch_chain2(ctx, local_start(ctx), EPI_CORRECT));
     for (int i = sweep2_ok(ctx) ? ctx->count : local_start(ctx); i < ctx->count; ++i) {
@@ -1842,10 +1910,17 @@ int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist) {
 }
 
 int prs_get_slice(prs_ctx *ctx, int n, double *out, int out_on_device) {
-    if (!ctx || !out) return PRS_EINVAL;
-    const int i = n - ctx->first;
-    if (i < 0 || i > ctx->count) { ctx->err = "slice not owned by this rank"; return PRS_EINVAL; }
-    CK(cudaMemcpyAsync(out, state(ctx, ctx->traj, i), ctx->sbytes,
+    if (!ctx || !out || n < 0 || n > ctx->p.N) return PRS_EINVAL;
+    const double *src = nullptr;
+    if (ctx->cyclic) {  // U_n is slice n's start (rank n mod P) and slice n-1's end state
+        if (n < ctx->p.N && n % ctx->nranks == ctx->rank) src = state(ctx, ctx->traj, n / ctx->nranks);
+        else if (n > 0 && (n - 1) % ctx->nranks == ctx->rank) src = state(ctx, ctx->tend, (n - 1) / ctx->nranks);
+    } else {
+        const int i = n - ctx->first;
+        if (i >= 0 && i <= ctx->count) src = state(ctx, ctx->traj, i);
+    }
+    if (!src) { ctx->err = "slice not owned by this rank"; return PRS_EINVAL; }
+    CK(cudaMemcpyAsync(out, src, ctx->sbytes,
                        out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return PRS_OK;
@@ -1937,6 +2012,10 @@ int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands) {
     const int n = ctx->p.n;
     const int P = (ctx->nranks > 1) ? ctx->nranks : bands;
     const bool pow2 = P >= 1 && (P & (P - 1)) == 0 && (n & (n - 1)) == 0;
+    if (ctx->cyclic) {
+        ctx->err = "space-parallel G: contiguous slice ownership only";
+        return PRS_EUNSUPPORTED;
+    }
     if (ctx->p.dim != 2 || ctx->p.split != 0 || ctx->p.G != PRS_FIE || !pow2 || n > 4096 || n % (L5RB * P) != 0 ||
         (long long)n * n / P < 4096) {
         ctx->err = "space-parallel G: 2-D dimensional split, G = FIE, P a power of two, n a power of two "
@@ -1970,6 +2049,45 @@ int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands) {
     CK(cudaMalloc(&ctx->gb_tot, sizeof(double) * 5 * (size_t)n * P));
     CK(cudaMalloc(&ctx->gb_yx, sizeof(double) * 2 * (size_t)n * P));
     ctx->gpar = 1;
+    return PRS_OK;
+}
+
+int prs_set_ownership(prs_ctx *ctx, int mode) {
+    if (!ctx || (mode != 0 && mode != 1)) return PRS_EINVAL;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (mode == 1 && (ctx->gpar || ctx->pipe)) {
+        ctx->err = "cyclic ownership: owner-G coarse chain, unpipelined (prs_set_coarse_mode 0, prs_set_pipeline 0)";
+        return PRS_EUNSUPPORTED;
+    }
+    const int cyc = (mode == 1 && ctx->nranks > 1) ? 1 : 0;  // one rank: the same layout either way
+    if (cyc == ctx->cyclic) return PRS_OK;
+    int first = 0, count = 0;
+    if (cyc) {
+        first = ctx->rank;
+        count = (ctx->p.N - ctx->rank + ctx->nranks - 1) / ctx->nranks;
+    } else {
+        prs_partition(ctx->p.N, ctx->nranks, ctx->rank, &first, &count);
+    }
+    const size_t sb = sizeof(double) * (size_t)ctx->ss;
+    double **bufs[] = {&ctx->traj, &ctx->fa, &ctx->fb, &ctx->gcache, &ctx->tend};
+    for (double **b : bufs)
+        if (*b) {
+            CK(cudaFree(*b));
+            *b = nullptr;
+        }
+    CK(cudaMalloc(&ctx->traj, sb * (count + 1)));
+    CK(cudaMalloc(&ctx->fa, sb * count));
+    CK(cudaMalloc(&ctx->fb, sb * count));
+    CK(cudaMalloc(&ctx->gcache, sb * count));
+    if (cyc) CK(cudaMalloc(&ctx->tend, sb * count));
+    ctx->cyclic = cyc;
+    ctx->first = first;
+    ctx->count = count;
+    ctx->delta = nullptr;
+    ctx->have_coarse = false;
+    if (ctx->have_initial && ctx->rank == 0)
+        CK(cudaMemcpyAsync(ctx->traj, ctx->u0, ctx->sbytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return PRS_OK;
 }
 

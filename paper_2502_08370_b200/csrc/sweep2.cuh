@@ -46,6 +46,7 @@ struct SWArgs {
     double tau, h2inv, creact, src_amp;
     const double *sinpi;
     long long slice0;     // global slice index of batch state 0
+    long long sstride;    // global slice stride between batch states (1; P under cyclic ownership)
     double dt;
     CoefTab tab;          // kappa = 1 pivots of (I - tau A_d), length n
 };
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
             for (int i = 0; i < LCH; ++i) v[i] = DR ? p[i] + w[k][i] : p[i];
             if (SRC) {
                 const double t = CHAIN ? (double)(a.slice0 + j + 1) * a.dt
-                                       : (double)((a.slice0 + b) * a.s + j + 1) * a.dt;
+                                       : (double)((a.slice0 + b * a.sstride) * a.s + j + 1) * a.dt;
                 const double f = a.tau * a.src_amp * exp(-t) * __ldg(a.sinpi + r0 + r);
 #pragma unroll
                 for (int i = 0; i < LCH; ++i) v[i] = fma(f, __ldg(a.sinpi + c * LCH + i), v[i]);

@@ -65,12 +65,12 @@ def run_ranks(p, P, body, u0=None):
 
 
 def local_slices(ctx, p):
-    """This rank's slice end states U_{first+1} .. U_{first+count} (host)."""
+    """This rank's slice end states U_{n+1}, n over its slices (host)."""
     buf = np.empty((p.n,) * p.dim)
     res = {}
-    for n in range(ctx.first + 1, ctx.first + ctx.count + 1):
-        ctx.get_slice(n, buf)
-        res[n] = buf.copy()
+    for n in ctx.slices():
+        ctx.get_slice(n + 1, buf)
+        res[n + 1] = buf.copy()
     return res
 
 
@@ -81,8 +81,10 @@ def gather(results):
     return full
 
 
-def iterate_body(kmax, tol, explicit=False):
+def iterate_body(kmax, tol, explicit=False, cyclic=False):
     def body(ctx, r, u0):
+        if cyclic:
+            ctx.set_ownership(1)
         ctx.set_initial(u0)
         ctx.coarse_sweep()
         if explicit:  # prs_fine_sweep + prs_parareal_correct, unlagged
@@ -111,14 +113,16 @@ OWNER_CASES = [
 
 @pytest.mark.parametrize("p,Ps,tol", OWNER_CASES, ids=lambda x: x.label() if hasattr(x, "label") else str(x))
 def test_owner_g_over_local_ranks_is_bitwise_the_single_rank_run(p, Ps, tol, monkeypatch):
-    """Owner-G over P ranks (lagged stop test, and the unlagged explicit loop): k, the update
-    history and every slice end state equal the one-rank run bit for bit, and the one-rank run
-    matches the oracle (iterates through prs_iterate)."""
+    """Owner-G over P ranks -- contiguous slice blocks with the lagged and the unlagged stop
+    test and the explicit fine_sweep / correct loop, and cyclic ownership (slice n on rank
+    n mod P, NEXT-2) -- k, the update history and every slice end state equal the one-rank run bit
+    for bit, and the one-rank run matches the oracle."""
     one = run_ranks(p, 1, iterate_body(p.N, tol))[0]
     for P in Ps:
-        for mode in ("lagged", "unlagged", "explicit"):
+        for mode in ("lagged", "unlagged", "explicit", "cyclic", "cyclic-explicit"):
             monkeypatch.setenv("PRS_LAG", "0" if mode == "unlagged" else "1")
-            res = run_ranks(p, P, iterate_body(p.N, tol, explicit=(mode == "explicit")))
+            res = run_ranks(p, P, iterate_body(p.N, tol, explicit=mode.endswith("explicit"),
+                                               cyclic=mode.startswith("cyclic")))
             assert all(r["k"] == one["k"] for r in res), (P, mode, [r["k"] for r in res])
             assert all(r["hist"] == one["hist"] for r in res), (P, mode)
             full = gather(res)
@@ -199,3 +203,15 @@ def test_space_parallel_g_over_local_ranks_matches_oracle_and_reruns(p, P):
         for r in res:
             for k in range(p.N):
                 assert abs(r[run][1][k] - cupds[k]) <= TOL * max(1.0, cupds[k]), (run, k)
+
+
+def test_cyclic_ownership_balances_the_active_slices():
+    """With converged-slice skipping contiguous blocks leave the first ranks idle
+    while the last keeps N/P slices; cyclic ownership keeps ceil((N - k)/P) per rank.  Host-side
+    check of the ownership rule the library implements (slice n on rank n mod P)."""
+    N, P = 64, 8
+    for k in (0, 9, 14, 40, 63):
+        active = [sum(1 for n in range(r, N, P) if n >= k) for r in range(P)]
+        assert max(active) - min(active) <= 1 and sum(active) == N - k
+        blocks = [max(0, min(N, (r + 1) * N // P) - max(k, r * N // P)) for r in range(P)]
+        assert max(blocks) == N // P  # the last block never shrinks before k > N - N/P
