@@ -68,7 +68,7 @@ def test_create_rejects_invalid_configs_before_touching_the_gpu():
             prs.Context(p)
         assert ei.value.code == prs.PRS_EINVAL
     for p in [synth.Problem(dim=3, G=synth.DR), synth.Problem(dim=3, coef=1),
-              synth.Problem(coef=2, split=1, n=32, dd_strips=4, dd_overlap=4)]:
+              synth.Problem(coef=2, split=0, n=32)]:  # mixed derivatives: DD split only
         with pytest.raises(prs.PrsError) as ei:
             prs.Context(p)
         assert ei.value.code == prs.PRS_EUNSUPPORTED
