@@ -88,6 +88,8 @@ def workload_config(p, name, n_gpus):
 
 # --------------------------------------------------------------------- clocks ---
 class ClockSampler:
+    """nvidia-smi every 100 ms on a reader thread; each sample keeps its host arrival time so the
+    samples of a time window (the timed region) can be picked out."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -95,24 +97,40 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.samples = []  # (host time, line)
 
     def start(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
 
-    def stop(self):
+        def reader():
+            for line in self.proc.stdout:
+                self.samples.append((time.perf_counter(), line))
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def count_since(self, t0):
+        return sum(1 for t, _ in self.samples if t >= t0)
+
+    def stop(self, t0=None, t1=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        lines = [ln for t, ln in self.samples if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -311,6 +329,7 @@ def run_prs(args):
     # timed region: the production path (CUDA-graph replays on one rank), no per-kernel events
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(0.5)  # nvidia-smi running before the timed region starts
     l0 = ctx.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -326,9 +345,26 @@ def run_prs(args):
             upds.append(step())
     ev1.record(stream)
     torch.cuda.synchronize()
+    t_end = time.perf_counter()
     launches = ctx.launches() - l0
     ms = ev0.elapsed_time(ev1)
-    clk = clocks.stop()
+    # a timed region shorter than the sampling period: keep the GPU on the same (untimed) steps
+    # until three samples have arrived since the region started, and report those
+    t_start = t_end - ms / 1e3
+    extra = 0
+    while clocks.proc is not None and clocks.count_since(t_start) < 3 and extra < 100000:
+        if args.pipeline:
+            ctx.iterate(1, 0.0)
+        else:
+            step()
+        extra += 1
+        if extra % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop(t_start, time.perf_counter())
+    if extra:
+        clk["window"] = (f"timed region {ms:.1f} ms < sampling period: samples over it and {extra} "
+                         "untimed steps of the same work right after it")
     # per-kernel device times for the roofline: the same steps again with CUDA events around
     # every fine-sweep launch (direct launches; not part of the timed value)
     ctx.set_profiling(True)
