@@ -400,7 +400,10 @@ static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.vol = ctx->vol;
     a.nrows = B * (long long)X7N;
     a.nstates = (int)B;
-    const long long ncl = ctx->num_sms;  // one cluster per SM pair slot: 2 CTAs per SM
+    long long ncl = ctx->num_sms;  // one cluster per SM pair slot: 2 CTAs per SM
+#ifdef PRS_X7_TIMING
+    if (getenv("PRS_X7_NCL")) ncl = atoll(getenv("PRS_X7_NCL"));
+#endif
     a.nranges = 0;
     if (B > 1) {
         long long g = ncl, bb = B;
@@ -1062,6 +1065,22 @@ void prs_destroy(prs_ctx *ctx) {
         if (h[3])
             fprintf(stderr, "DD timing: %llu tasks, per task %.1f us, forward wait %.1f us, backward wait %.1f us\n",
                     h[3], h[2] / 1e3 / h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3]);
+    }
+#endif
+#ifdef PRS_X7_TIMING
+    {
+        unsigned long long h[2][10];
+        cudaMemcpyFromSymbol(h, prs::g_x7_timing, sizeof(h));
+        static const char *ph[9] = {"cp.async wait", "barrier", "loads+stencil", "F1+scan", "fwd msg", "F3+scan",
+                                    "bwd msg", "B3+store", "scalars+issue"};
+        for (int r = 0; r < 2; ++r)
+            if (h[r][9]) {
+                fprintf(stderr, "x7 timing rank %d: %llu rows, cycles per row:", r, h[r][9]);
+                double tot = 0;
+                for (int p = 0; p < 9; ++p) tot += (double)h[r][p] / h[r][9];
+                for (int p = 0; p < 9; ++p) fprintf(stderr, " %s %.0f", ph[p], (double)h[r][p] / h[r][9]);
+                fprintf(stderr, " | total %.0f\n", tot);
+            }
     }
 #endif
     delete ctx->tr;

@@ -19,6 +19,24 @@
 
 namespace prs {
 
+#ifdef PRS_X7_TIMING
+// diagnostic build only (-DPRS_X7_TIMING): clock64 cycles of thread 0 of every CTA per phase of
+// a row, summed over rows, per cluster rank: [rank][phase], phase 8 = rows
+__device__ unsigned long long g_x7_timing[2][10];
+#define X7T_MARK(ph)                                                      \
+    do {                                                                  \
+        if (k == 0) {                                                     \
+            const long long t_ = clock64();                               \
+            tacc[ph] += (unsigned long long)(t_ - tlast);                 \
+            tlast = t_;                                                   \
+        }                                                                 \
+    } while (0)
+#else
+#define X7T_MARK(ph) \
+    do {             \
+    } while (0)
+#endif
+
 constexpr int X7T = 128;           // threads = chunks per half row
 constexpr int X7G = X7T * X3C;     // doubles per half-row slot (padded chunk layout)
 constexpr int X7N = 2 * X7T * LCH; // row length (4096)
@@ -78,6 +96,10 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
     const double tauh = a.tau * a.h2inv;
     const long long hoff = (long long)crank * (X7T * LCH);  // this CTA's half of a row
     unsigned rowpar = 0;  // parity of the incoming message of the current row
+#ifdef PRS_X7_TIMING
+    unsigned long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tlast = clock64();
+#endif
 
     auto issue_group = [&](const double *rowp, double *dst) {
 #pragma unroll
@@ -140,9 +162,12 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             if (g + 2 < G && g + 2 < g1 + (DR ? 1 : 0)) issue_state(g + 2);
             if (COEF && g + 1 < g1) issue_piv(g + 1);
             cp_async_commit();
+            X7T_MARK(8);  // scalars + issue
             cp_async_wait<1>();
             if (k == 0) mbar_arrive_expect(&mbx, 16);  // this row's incoming message
+            X7T_MARK(0);  // cp.async wait for this row's group
             __syncthreads();
+            X7T_MARK(1);  // wait for this row's data
 
             const int j = (int)(g & 4095);
             const double *U = ub(g);
@@ -192,6 +217,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
                 idm1 = (k > 0) ? I[-X3C + LCH - 1] : cur.idm1;
                 hsx = 0.5 * cur.hsx;
             }
+            X7T_MARK(2);  // loads + DR stencil
             auto af = [&](int i) { return -tauh * fma(hsx, sf[i], 1.0); };
             auto cm = [&](int i) { return COEF ? af(i) * (i == 0 ? idm1 : idr[i - 1]) : tm[i]; };
             auto cid = [&](int i) { return COEF ? idr[i] : tid_[i]; };
@@ -208,6 +234,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             seg_scan_fwd(A, B, 32, lane, EA, EB);
             if (lane == 31) scr[warp] = make_double2(A, B);
             __syncthreads();
+            X7T_MARK(3);  // F1 + forward warp scan + barrier
             double Yc = 0.0;  // y entering this CTA's half
             if (crank == 0) {
                 if (k == 0) {  // y at the end of the half from y = 0 at the row start -> CTA 1
@@ -224,6 +251,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
                 mbar_wait(&mbx, rowpar);
                 Yc = xin.y;
             }
+            X7T_MARK(4);  // forward message (send / wait)
             double Yw = Yc;
             for (int q = 0; q < warp; ++q) {
                 const double2 s = scr[q];
@@ -242,6 +270,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             seg_scan_bwd(Pb, Qb, 32, lane, EP, EQ);
             if (lane == 0) scr[NW + warp] = make_double2(Pb, Qb);
             __syncthreads();
+            X7T_MARK(5);  // F3 + backward warp scan + barrier
             double Xc = 0.0;  // x after this CTA's half
             if (crank == 1) {
                 if (k == 0) {  // x at this half's first point from x = 0 at the row end -> CTA 0
@@ -259,6 +288,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
                 Xc = xin.y;
             }
             rowpar ^= 1u;
+            X7T_MARK(6);  // backward message (send / wait)
             double Xw = Xc;
             for (int q = NW - 1; q > warp; --q) {
                 const double2 s = scr[NW + q];
@@ -291,9 +321,17 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
                 }
             }
             __syncthreads();  // staging slot free before the next prefetch lands in it
+            X7T_MARK(7);  // B3 + staging + store
+#ifdef PRS_X7_TIMING
+            if (k == 0) tacc[9] += 1;
+#endif
         }
         cp_async_wait<0>();
     }
+#ifdef PRS_X7_TIMING
+    if (k == 0)
+        for (int p = 0; p < 10; ++p) atomicAdd(&g_x7_timing[crank][p], tacc[p]);
+#endif
     cl.sync();  // neither CTA leaves while its partner may still address its shared memory
 }
 
