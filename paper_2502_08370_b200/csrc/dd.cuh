@@ -206,11 +206,16 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, i
         const double th = C[a * W + a];
         theta[a] = th;
         const double bd = th + 2.0 * s;
-        double d = bd;
+        double d = bd, prev = 0.0;
+        int lc = 0;  // last row whose pivot differs from the row before: rows >= lc share one value
         for (int l = 0; l < n; ++l) {
             if (l > 0) d = bd - s * s / d;
-            idy[(long long)l * W + a] = 1.0 / d;
+            const double id = 1.0 / d;
+            if (l > 0 && id != prev) lc = l;
+            prev = id;
+            idy[(long long)l * W + a] = id;
         }
+        theta[W + a] = (double)lc;  // (the recurrence reaches its fixed point in a few hundred rows)
     }
     for (int e = tid; e < W * W; e += blockDim.x) {
         const int r = e / W, k = e % W;
@@ -231,6 +236,7 @@ struct DDStageArgs {
     int nblk;            // blocks of this colour
     const int *bi0, *bW; // block column start / width
     const double *const *Q, *const *QT, *const *idy;  // per block
+    const double *const *conv;  // per block [W]: pivots of mode a are equal from this row on
     double tau, h2inv, c;
     const double *rhon, *rhof;  // rho tables (colour 0 then colour 1)
     double src_amp;
@@ -248,17 +254,40 @@ struct DDStageArgs {
     int *gflag;
     double2 *gtot;
     int ntasks;
+    // split stage (dd_p1 / dd_scan / dd_p2): per task the transformed tile G [R][DD_WMAX], the
+    // piece's transfer tuple [5][DD_WMAX] and its boundary values y_in, x_in [2][DD_WMAX]
+    double *gs, *tup, *bnd;
+    int abl;  // diagnostic build (-DPRS_DD_TIMING) only: PRS_DD_ABL bit 0 skips the GEMMs, bit 1 the walks
 };
 
 #ifdef PRS_DD_TIMING
 // diagnostic build only (-DPRS_DD_TIMING): per task, ns spent waiting for the forward / the
 // backward scan totals of the other row pieces, the task's duration, and the task count
 __device__ unsigned long long g_dd_timing[4];
+// split stage: per task (thread 0) ns in p1 load / GEMM / G store + walk, p2 load / walk / GEMM /
+// store, and the task counts of p1, p2
+__device__ unsigned long long g_dd2_timing[9];
+#define DD2T(i)                                                   \
+    do {                                                          \
+        if (threadIdx.x == 0) {                                   \
+            const unsigned long long t_ = dd_gtimer();            \
+            atomicAdd(&g_dd2_timing[i], t_ - tt_);                \
+            tt_ = t_;                                             \
+        }                                                         \
+    } while (0)
+#define DD2T0 unsigned long long tt_ = dd_gtimer()
 __device__ __forceinline__ unsigned long long dd_gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#else
+#define DD2T(i) \
+    do {        \
+    } while (0)
+#define DD2T0 \
+    do {      \
+    } while (0)
 #endif
 
 // L2-scope flag hand-off between CTAs (GX): release after the CTA's total is written, acquire
@@ -419,32 +448,31 @@ __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, 
 // GX = 0: the CL pieces are the CTAs of one cluster and exchange their scan totals through
 // distributed shared memory; GX = 1: the pieces are independent tasks of a persistent grid and
 // exchange them through L2 (per-task flags), see dd_stage_kernel.
-template <int DR, int SRC, int GX>
-__device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, long long task, int crank) {
-    double *T = sh;                                          // (cpad(R-1)+1) x DD_WPAD
-    double *Ms = sh + (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // 2 x DD_KC x DD_WPAD (GEMM)
-    double2 *sc = reinterpret_cast<double2 *>(Ms);           // 8 x DD_WMAX chunk maps (y solve)
-    double2 *ctf = reinterpret_cast<double2 *>(Ms + 2 * DD_KC * DD_WPAD);  // cluster totals fwd
-    double2 *ctb = ctf + DD_WMAX;                             // cluster totals bwd
-    const long long tk = task * a.CL + crank;                 // GX slot
-    double2 *gtf = a.gtot + tk * 2 * DD_WMAX, *gtb = gtf + DD_WMAX;
+// Barrier of the threads working on one tile (the whole CTA).
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
 
-    const int tid = threadIdx.x;
-    const int blk = (int)(task % a.nblk);
-    const long long b = task / a.nblk;
+// Per-lane column masks of a tile (lane owns columns lane + 32 k): done0m -- already final
+// after stage 0 (stage 1 takes them from V); finm -- final after this stage (epilogue applies).
+struct DDCols {
+    unsigned done0m, finm;
+};
+
+// Load the right-hand side tile of rows r0 .. r0 + nrow - 1 of block blk of state b into the
+// chunk-padded shared tile T (columns >= W zero): one row per warp, columns across lanes.
+template <int DR, int SRC, int NT = DD_THREADS, class SY = CtaSync>
+__device__ __forceinline__ DDCols dd_load_tile(const DDStageArgs &a, double *T, long long b, int blk, int r0,
+                                               int nrow, int tid = threadIdx.x, SY sync = SY{}) {
     const int i0 = a.bi0[blk], W = a.bW[blk];
     const int n = a.n;
-    const int r0 = crank * a.R;
-    const int nrow = max(0, min(a.R, n - r0));
     const double *Ub = a.U + b * a.vol;
-    double *Vb = a.V + b * a.vol;
+    const double *Vb = a.V + b * a.vol;
     const int me = a.stage, other = 1 - a.stage;
     const double *rn_ot = a.rhon + other * n, *rf_ot = a.rhof + other * (n + 1);
     double ampt = 0.0;
     if (SRC) ampt = a.src_amp * exp(-src_time(a.ta, b));
-
-    // ---- load the right-hand side tile: one row per warp, columns across lanes; every
-    // global load of a row is issued before the first use (several rows' worth in flight) ----
+    // every global load of a row is issued before the first use (several rows' worth in flight)
     constexpr int NCW = (DD_WMAX + 31) / 32;  // column slots per lane
     // per-lane column constants, loaded once: the source profile and, for stage 1, which
     // columns are already final after stage 0 (rho_0 > 0)
@@ -459,14 +487,71 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
         if (me == 1 && pos) done0m |= 1u << k;
         if (ci < W && (me == 1 || !pos)) finm |= 1u << k;
     }
+    if (!(DR && me == 0)) {
+        // no stencil: asynchronous 8-byte copies of the raw rows (stage 1: V on the columns that
+        // are final after stage 0, U elsewhere), every one of the tile in flight at once; the
+        // source term is added in shared memory after they land
+        const int wp = tid >> 5, ln = tid & 31;
+        if (((n | i0 | W) & 1) == 0) {
+            // 16-byte copies of column pairs (both columns from the same source: V where rho_0 > 0,
+            // which holds pairwise here -- else two 8-byte copies)
+            const double *rn0 = a.rhon;  // colour 0
+            for (int rl = wp; rl < nrow; rl += (NT / 32)) {
+                const long long g0 = (long long)(r0 + rl) * n + i0;
+                double *trow = T + cpad(rl) * DD_WPAD;
+#pragma unroll
+                for (int k = 0; k < (DD_WMAX / 2 + 31) / 32; ++k) {
+                    const int ci = 2 * (ln + 32 * k);
+                    if (ci < W) {
+                        const bool v0 = me == 1 && rn0[i0 + ci] > 0.0, v1 = me == 1 && rn0[i0 + ci + 1] > 0.0;
+                        if (v0 == v1) {
+                            cp_async16(trow + ci, (v0 ? Vb : Ub) + g0 + ci);
+                        } else {
+                            cp_async8(trow + ci, (v0 ? Vb : Ub) + g0 + ci);
+                            cp_async8(trow + ci + 1, (v1 ? Vb : Ub) + g0 + ci + 1);
+                        }
+                    } else if (ci < DD_WMAX) {
+                        trow[ci] = 0.0;
+                        trow[ci + 1] = 0.0;
+                    }
+                }
+            }
+        } else {
+            for (int rl = wp; rl < nrow; rl += (NT / 32)) {
+                const long long g0 = (long long)(r0 + rl) * n + i0;
+                double *trow = T + cpad(rl) * DD_WPAD;
+#pragma unroll
+                for (int k = 0; k < NCW; ++k) {
+                    const int ci = ln + 32 * k;
+                    if (ci < W) cp_async8(trow + ci, (((done0m >> k) & 1u) ? Vb : Ub) + g0 + ci);
+                    else if (ci < DD_WMAX) trow[ci] = 0.0;
+                }
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        sync();
+        if (SRC) {
+            for (int rl = wp; rl < nrow; rl += (NT / 32)) {
+                const double sl = a.tau * ampt * __ldg(a.sinpi + r0 + rl);
+                double *trow = T + cpad(rl) * DD_WPAD;
+#pragma unroll
+                for (int k = 0; k < NCW; ++k) {
+                    const int ci = ln + 32 * k;
+                    if (ci < W && !((done0m >> k) & 1u)) trow[ci] += sl * spk[k];
+                }
+            }
+        }
+        return DDCols{done0m, finm};
+    }
     {
         const int wp = tid >> 5, ln = tid & 31;
         // the source profile of the warp's rows wp + 16 q, one per lane (q = lane), shuffled out
-        static_assert(DD_RMAX / (DD_THREADS / 32) <= 32, "rows per warp");
+        static_assert(DD_RMAX / ((NT / 32)) <= 32, "rows per warp");
         double slq = 0.0;
-        if (SRC && wp + (DD_THREADS / 32) * ln < nrow) slq = a.tau * ampt * __ldg(a.sinpi + r0 + wp + (DD_THREADS / 32) * ln);
+        if (SRC && wp + ((NT / 32)) * ln < nrow) slq = a.tau * ampt * __ldg(a.sinpi + r0 + wp + ((NT / 32)) * ln);
 #pragma unroll 2
-        for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
+        for (int rl = wp; rl < nrow; rl += (NT / 32)) {
             const int l = r0 + rl;
             const long long g0 = (long long)l * n + i0;
             double r[NCW], u[NCW];
@@ -500,7 +585,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
                     }
                 }
             }
-            const double sl = SRC ? __shfl_sync(0xffffffffu, slq, (rl - wp) / (DD_THREADS / 32)) : 0.0;
+            const double sl = SRC ? __shfl_sync(0xffffffffu, slq, (rl - wp) / ((NT / 32))) : 0.0;
 #pragma unroll
             for (int k = 0; k < NCW; ++k) {
                 const int ci = ln + 32 * k, i = i0 + ci;
@@ -521,6 +606,98 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
             }
         }
     }
+    return DDCols{done0m, finm};
+}
+
+// Store the solved tile (V = x [DR stage 0: - w]) with the fused parareal epilogue on the values
+// that are final after this stage: one row per warp.
+template <int DR, int NT = DD_THREADS>
+__device__ __forceinline__ void dd_store_tile(const DDStageArgs &a, const double *T, long long b, int blk, int r0,
+                                              int nrow, unsigned finm, int tid = threadIdx.x) {
+    const int lane = tid & 31;
+    const int i0 = a.bi0[blk], W = a.bW[blk];
+    const int n = a.n;
+    const double *Ub = a.U + b * a.vol;
+    double *Vb = a.V + b * a.vol;
+    const int me = a.stage, other = 1 - a.stage;
+    const double *rn_ot = a.rhon + other * n, *rf_ot = a.rhof + other * (n + 1);
+    constexpr int NCW = (DD_WMAX + 31) / 32;
+    double dmax = 0.0;
+    unsigned long long bad = 0;
+    {
+        const int wp = tid >> 5;
+        for (int rl = wp; rl < nrow; rl += (NT / 32)) {
+            const int l = r0 + rl;
+            const long long g0 = (long long)l * n + i0;
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) {
+                const int ci = lane + 32 * k, i = i0 + ci;
+                if (ci >= W) continue;
+                const long long g = g0 + ci;
+                double x = T[cpad(rl) * DD_WPAD + ci];
+                if (DR && me == 0) {  // V = x - w
+                    const double u = Ub[g];
+                    const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
+                    const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
+                    const double rnode = rn_ot[i];
+                    x -= a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) + rnode * (vp - 2.0 * u + vm)) *
+                                      a.h2inv -
+                                  rnode * a.c * u);
+                }
+                const bool final_here = (finm >> k) & 1u;
+                const int ep = final_here ? a.epi : EPI_STORE;
+                const long long gb = b * a.vol + g;
+                if (ep == EPI_STORE) {
+                    Vb[g] = x;
+                } else if (ep == EPI_DELTA) {
+                    Vb[g] = x - a.e_gc[gb];
+                } else if (ep == EPI_CORRECT) {
+                    const double nv = x + a.e_delta[g];
+                    const double ov = a.e_traj[g];
+                    a.e_gcache[g] = x;
+                    a.e_traj[g] = nv;
+                    dmax = fmax(dmax, fabs(nv - ov));
+                    if (!isfinite(nv)) bad = 1;
+                } else {  // INIT
+                    a.e_gcache[g] = x;
+                    a.e_traj[g] = x;
+                }
+            }
+        }
+    }
+    if (a.epi == EPI_CORRECT) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, off);
+        }
+        if (lane == 0) {
+            atomicMax(a.e_red, (unsigned long long)__double_as_longlong(dmax));
+            if (bad) atomicOr(a.e_red + 1, 1ull);
+        }
+    }
+}
+
+template <int DR, int SRC, int GX>
+__device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, long long task, int crank) {
+    double *T = sh;                                          // (cpad(R-1)+1) x DD_WPAD
+    double *Ms = sh + (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // 2 x DD_KC x DD_WPAD (GEMM)
+    double2 *sc = reinterpret_cast<double2 *>(Ms);           // 8 x DD_WMAX chunk maps (y solve)
+    double2 *ctf = reinterpret_cast<double2 *>(Ms + 2 * DD_KC * DD_WPAD);  // cluster totals fwd
+    double2 *ctb = ctf + DD_WMAX;                             // cluster totals bwd
+    const long long tk = task * a.CL + crank;                 // GX slot
+    double2 *gtf = a.gtot + tk * 2 * DD_WMAX, *gtb = gtf + DD_WMAX;
+
+    const int tid = threadIdx.x;
+    const int blk = (int)(task % a.nblk);
+    const long long b = task / a.nblk;
+    const int i0 = a.bi0[blk], W = a.bW[blk];
+    const int n = a.n;
+    const int r0 = crank * a.R;
+    const int nrow = max(0, min(a.R, n - r0));
+
+    const DDCols cols = dd_load_tile<DR, SRC>(a, T, b, blk, r0, nrow);
+
     // ---- G = F Q ----
     dd_tile_gemm(T, a.Q[blk], W, nrow, Ms);
 
@@ -769,61 +946,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
     // ---- U = V Q^T ----
     dd_tile_gemm(T, a.QT[blk], W, nrow, Ms);
 
-    // ---- store (+ fused parareal epilogue for final values): one row per warp ----
-    double dmax = 0.0;
-    unsigned long long bad = 0;
-    {
-        const int wp = tid >> 5;
-        for (int rl = wp; rl < nrow; rl += DD_THREADS / 32) {
-            const int l = r0 + rl;
-            const long long g0 = (long long)l * n + i0;
-#pragma unroll
-            for (int k = 0; k < NCW; ++k) {
-                const int ci = lane + 32 * k, i = i0 + ci;
-                if (ci >= W) continue;
-                const long long g = g0 + ci;
-                double x = T[cpad(rl) * DD_WPAD + ci];
-                if (DR && me == 0) {  // V = x - w
-                    const double u = Ub[g];
-                    const double um = (i > 0) ? Ub[g - 1] : 0.0, up = (i < n - 1) ? Ub[g + 1] : 0.0;
-                    const double vm = (l > 0) ? Ub[g - n] : 0.0, vp = (l < n - 1) ? Ub[g + n] : 0.0;
-                    const double rnode = rn_ot[i];
-                    x -= a.tau * ((rf_ot[i + 1] * (up - u) - rf_ot[i] * (u - um) + rnode * (vp - 2.0 * u + vm)) *
-                                      a.h2inv -
-                                  rnode * a.c * u);
-                }
-                const bool final_here = (finm >> k) & 1u;
-                const int ep = final_here ? a.epi : EPI_STORE;
-                const long long gb = b * a.vol + g;
-                if (ep == EPI_STORE) {
-                    Vb[g] = x;
-                } else if (ep == EPI_DELTA) {
-                    Vb[g] = x - a.e_gc[gb];
-                } else if (ep == EPI_CORRECT) {
-                    const double nv = x + a.e_delta[g];
-                    const double ov = a.e_traj[g];
-                    a.e_gcache[g] = x;
-                    a.e_traj[g] = nv;
-                    dmax = fmax(dmax, fabs(nv - ov));
-                    if (!isfinite(nv)) bad = 1;
-                } else {  // INIT
-                    a.e_gcache[g] = x;
-                    a.e_traj[g] = x;
-                }
-            }
-        }
-    }
-    if (a.epi == EPI_CORRECT) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
-            bad |= __shfl_xor_sync(0xffffffffu, bad, off);
-        }
-        if (lane == 0) {
-            atomicMax(a.e_red, (unsigned long long)__double_as_longlong(dmax));
-            if (bad) atomicOr(a.e_red + 1, 1ull);
-        }
-    }
+    dd_store_tile<DR>(a, T, b, blk, r0, nrow, cols.finm);
 }
 
 // GX = 0: one CTA per task piece, clusters of CL CTAs.  GX = 1: a persistent grid (one CTA per
@@ -859,6 +982,397 @@ __global__ void __launch_bounds__(DD_THREADS, 2) dd_stage_kernel(DDStageArgs a) 
     }
 }
 
+// GEMM of the split stage: T[l][:] <- T[l][:] . M for every row of the tile, in place, on DMMA
+// (m8n8k4 f64), without shared staging of M or barriers inside the k loop.  Warp w owns output
+// columns 16 w .. 16 w + 15 for all DD_RMAX rows (8 x 2 tiles of 8 x 8, accumulators in
+// registers): its B fragments (M[k][c], k = lane % 4, c = lane / 4) are read straight from
+// global memory (L2-resident; no other warp of the CTA needs them) DD2_PF k-steps ahead of use,
+// its A fragments (T[r][k], r = lane / 4) from the shared tile.  Rows >= nrow compute and
+// discard; columns >= W of T are zero and B is zero outside the W x W matrix.
+constexpr int DD2_THREADS = 32 * (DD_WMAX / 16);  // 9 warps
+constexpr int DD_SUB = DD_RMAX / 2;                // rows of a walk sub-piece (two per tile)
+static_assert(DD2_THREADS >= 2 * DD_WMAX, "two walking threads per mode");
+constexpr int DD2_PF = 3;
+template <class SY>
+__device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restrict__ M, int W, int tid, SY sync) {
+    static_assert(DD_RMAX == 64 && DD_WMAX % 16 == 0, "dmma tiling of the split stage");
+    const int lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fk = lane & 3, cb = 16 * warp;
+    const bool active = cb < W;  // warp-uniform
+    double acc[8][2][2];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+    sync();  // the tile is complete
+    if (active) {
+        const int c0 = cb + fr, c1 = cb + 8 + fr;
+        const bool v0 = c0 < W, v1 = c1 < W;
+        const int nks = (W + 3) / 4;
+        double b0[DD2_PF], b1[DD2_PF];
+        auto ldb = [&](int ks, double &x0, double &x1) {
+            const int k = 4 * ks + fk;
+            const bool kin = k < W;
+            x0 = (kin && v0) ? __ldg(M + (long long)k * W + c0) : 0.0;
+            x1 = (kin && v1) ? __ldg(M + (long long)k * W + c1) : 0.0;
+        };
+#pragma unroll
+        for (int q = 0; q < DD2_PF; ++q) ldb(q, b0[q], b1[q]);
+        const double *ta = T + fk;
+        for (int ks0 = 0; ks0 < nks; ks0 += DD2_PF) {
+#pragma unroll
+            for (int q = 0; q < DD2_PF; ++q) {
+                const int ks = ks0 + q;
+                if (ks < nks) {
+                    const double bb0 = b0[q], bb1 = b1[q];
+                    ldb(ks + DD2_PF, b0[q], b1[q]);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const double av = ta[cpad(8 * r + fr) * DD_WPAD + 4 * ks];
+                        dmma_f64(acc[r][0][0], acc[r][0][1], av, bb0);
+                        dmma_f64(acc[r][1][0], acc[r][1][1], av, bb1);
+                    }
+                }
+            }
+        }
+    }
+    sync();  // every read of the tile is done: write in place
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col = cb + 8 * c + 2 * fk;
+                double *p = T + cpad(8 * r + fr) * DD_WPAD + col;
+                if (col < W) p[0] = acc[r][c][0];
+                if (col + 1 < W) p[1] = acc[r][c][1];
+            }
+    }
+    sync();
+}
+
+// ------------------------------------------------------- split stage (default path) ----
+// The same stage as two passes over every block's row pieces with a scan between them, so that
+// no piece waits on another (in dd_stage_task the scan-total exchange and the barriers behind it
+// cost ~30 % of the stall samples, profiles/r02_ncu_dd_fine_summary.txt):
+//   dd_p1_kernel: load + G = F Q (DMMA); store G; per mode a, over the piece's rows, the transfer
+//     tuple of the y recurrences from the piece's boundary values
+//        y_l     = alpha_l y_in + beta_l        (y_in: y at the row before the piece)
+//        x_first = P x_in + Q1 y_in + Q0        (x_in: x at the row after the piece)
+//     i.e. (A, B) = (alpha, beta) at the piece's last row, P the product of -cc, Q0 / Q1 the
+//     backward maps' weights applied to beta / alpha;
+//   dd_scan_kernel: per (state, block, mode) the y_in of every half piece (the walks run on
+//     half pieces, two threads per mode) in order, then x_in in reverse order;
+//   dd_p2_kernel: reload G, the exact forward recurrence from y_in and the backward one from
+//     x_in (the arithmetic of the F3 / B3 walks), U = V Q^T (DMMA), store with the epilogue.
+// Pieces are independent CTAs (two per SM): one piece's loads and walks overlap another's GEMM.
+
+// the walk's row coefficients: m_l = -tau/h^2 id_{l-1} (0 on the line's first row),
+// cc_l = -tau/h^2 id_l (0 on its last row), id_l = 1 / pivot (precomputed per mode, dd_factor_kernel)
+// The walking thread's scalars, loaded ahead of the walk (before the GEMM in pass 1, before the
+// wait for G in pass 2) so that their latency hides behind other work: the row from which the
+// mode's pivots are constant, that pivot, and (pass 2) the sub-piece's boundary values.
+struct DDWalkPre {
+    int lc;
+    double ids, yb, xb;
+};
+template <int P1>
+__device__ __forceinline__ DDWalkPre dd_walk_prefetch(const DDStageArgs &a, int blk, long long tk, int tid) {
+    DDWalkPre w{0, 0.0, 0.0, 0.0};
+    const int W = a.bW[blk], h = tid / DD_WMAX, am = tid - h * DD_WMAX;
+    if (am >= W || h > 1) return w;
+    w.lc = (int)__ldg(a.conv[blk] + am);
+    w.ids = __ldg(a.idy[blk] + am + (long long)(a.n - 1) * W);
+    if (!P1) {
+        const long long t2 = 2 * tk + h;
+        w.yb = a.bnd[t2 * 2 * DD_WMAX + am];
+        w.xb = a.bnd[(t2 * 2 + 1) * DD_WMAX + am];
+    }
+    return w;
+}
+
+template <int P1>
+__device__ __forceinline__ void dd_piece_walks(const DDStageArgs &a, double *T, int blk, int r0, int nrow,
+                                               long long tk, int tid, const DDWalkPre &wp) {
+    // Two threads per mode: thread (h, am) walks half h of the piece (sub-piece 2 tk + h, DD_SUB
+    // rows; the scan runs over sub-pieces), in batches of U rows: the batch's tile values are
+    // read into registers before the recurrence runs over them (no shared-memory latency inside
+    // the chain) and the next batch's pivots are in flight meanwhile.
+    const int W = a.bW[blk], n = a.n, h = tid / DD_WMAX, am = tid - h * DD_WMAX;
+    if (am >= W || h > 1) return;
+#ifdef PRS_DD_TIMING
+    if (a.abl & 2) return;
+#endif
+    const int rb = DD_SUB * h;  // first tile row of the sub-piece
+    r0 += rb;
+    nrow = max(0, min(DD_SUB, nrow - rb));
+    tk = 2 * tk + h;
+    const double ms = -a.tau * a.h2inv;
+    const double *idc = a.idy[blk] + am;
+    constexpr int U = 8;
+    // rows >= lc (most pieces of a long block) share the converged pivot: no loads there
+    const int lc = wp.lc;
+    const double ids = wp.ids;
+    auto ldid = [&](int rl) {
+        return (rl >= 0 && rl < nrow) ? (r0 + rl >= lc ? ids : __ldg(idc + (long long)(r0 + rl) * W)) : 0.0;
+    };
+    auto trow = [&](int rl) { return T + cpad(rb + rl) * DD_WPAD + am; };
+    double idn[U];
+    if (P1) {
+        double al = 1.0, be = 0.0, pr = 1.0, q0 = 0.0, q1 = 0.0;
+        double idp = (r0 > 0) ? (r0 - 1 >= lc ? ids : __ldg(idc + (long long)(r0 - 1) * W)) : 0.0;
+#pragma unroll
+        for (int i = 0; i < U; ++i) idn[i] = ldid(i);
+        for (int c0 = 0; c0 < nrow; c0 += U) {
+            double id[U], t[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                id[i] = idn[i];
+                idn[i] = ldid(c0 + U + i);
+                t[i] = (c0 + i < nrow) ? *trow(c0 + i) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i)
+                if (c0 + i < nrow) {
+                    const int l = r0 + c0 + i;
+                    const double m = (l == 0) ? 0.0 : ms * idp;
+                    const double cc = (l == n - 1) ? 0.0 : ms * id[i];
+                    be = fma(-m, be, t[i]);
+                    al = -m * al;
+                    const double wv = pr * id[i];
+                    q0 = fma(wv, be, q0);
+                    q1 = fma(wv, al, q1);
+                    pr *= -cc;
+                    idp = id[i];
+                }
+        }
+        double *tp = a.tup + tk * 5 * DD_WMAX + am;
+        tp[0] = al;
+        tp[DD_WMAX] = be;
+        tp[2 * DD_WMAX] = pr;
+        tp[3 * DD_WMAX] = q0;
+        tp[4 * DD_WMAX] = q1;
+    } else {
+        double y = wp.yb;
+        double idp = (r0 > 0) ? (r0 - 1 >= lc ? ids : __ldg(idc + (long long)(r0 - 1) * W)) : 0.0;
+#pragma unroll
+        for (int i = 0; i < U; ++i) idn[i] = ldid(i);
+        for (int c0 = 0; c0 < nrow; c0 += U) {
+            double id[U], t[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                id[i] = idn[i];
+                idn[i] = ldid(c0 + U + i);
+                t[i] = (c0 + i < nrow) ? *trow(c0 + i) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                const int l = r0 + c0 + i;
+                const double m = (l == 0) ? 0.0 : ms * idp;
+                y = fma(-m, y, t[i]);
+                t[i] = y;
+                idp = id[i];
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i)
+                if (c0 + i < nrow) *trow(c0 + i) = t[i];
+        }
+        // backward, from the piece's last row (the batches in reverse)
+        double x = wp.xb;
+#pragma unroll
+        for (int i = 0; i < U; ++i) idn[i] = ldid(nrow - 1 - i);
+        for (int c1 = nrow - 1; c1 >= 0; c1 -= U) {
+            double id[U], t[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                id[i] = idn[i];
+                idn[i] = ldid(c1 - U - i);
+                t[i] = (c1 - i >= 0) ? *trow(c1 - i) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                const int l = r0 + c1 - i;
+                const double ccv = (l == n - 1) ? 0.0 : ms * id[i];
+                x = fma(id[i], t[i], -ccv * x);
+                t[i] = x;
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i)
+                if (c1 - i >= 0) *trow(c1 - i) = t[i];
+        }
+    }
+}
+
+// A task of the split stage: row piece crank of block blk of state b (tk = (b nblk + blk) CL + crank).
+struct DDTask {
+    long long tk, task, b;
+    int crank, blk, W, r0, nrow;
+    __device__ __forceinline__ DDTask(const DDStageArgs &a, long long t) : tk(t), task(t / a.CL) {
+        crank = (int)(t % a.CL);
+        blk = (int)(task % a.nblk);
+        b = task / a.nblk;
+        W = a.bW[blk];
+        r0 = crank * a.R;
+        nrow = max(0, min(a.R, a.n - r0));
+    }
+};
+
+// pass 1 before its GEMM: the right-hand side tile
+template <int DR, int SRC, class SY>
+__device__ __forceinline__ void dd_p1_pre(const DDStageArgs &a, double *T, const DDTask &t, int tid, SY sync) {
+    dd_load_tile<DR, SRC, DD2_THREADS>(a, T, t.b, t.blk, t.r0, t.nrow, tid, sync);
+}
+// pass 1 after its GEMM: G to global (bulk copies by one thread while the walks read the tile),
+// the piece's transfer tuples; the tile is free again when this returns
+template <class SY>
+__device__ __forceinline__ void dd_p1_post(const DDStageArgs &a, double *T, const DDTask &t, int tid, SY sync,
+                                           const DDWalkPre &wp) {
+    double *G = a.gs + (t.task * a.n + t.r0) * (long long)DD_WMAX;
+    const bool bulk = (t.W & 1) == 0;  // rows of W doubles are 16-byte multiples
+    if (bulk) {
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            for (int rl = 0; rl < t.nrow; ++rl)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                                 G + (long long)rl * DD_WMAX),
+                             "r"(smem_u32(T + cpad(rl) * DD_WPAD)), "r"((unsigned)(t.W * sizeof(double)))
+                             : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    } else {
+        const int lane = tid & 31;
+        for (int rl = tid >> 5; rl < t.nrow; rl += DD2_THREADS / 32)
+#pragma unroll
+            for (int k = 0; k < (DD_WMAX + 31) / 32; ++k) {
+                const int ci = lane + 32 * k;
+                if (ci < t.W) G[(long long)rl * DD_WMAX + ci] = T[cpad(rl) * DD_WPAD + ci];
+            }
+    }
+    dd_piece_walks<1>(a, T, t.blk, t.r0, t.nrow, t.tk, tid, wp);
+    if (bulk && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    sync();
+}
+// pass 2 before its GEMM: G back (bulk copies completing on the group's mbarrier, phase `par`),
+// the exact recurrences of the piece from its boundary values
+template <class SY>
+__device__ __forceinline__ void dd_p2_pre(const DDStageArgs &a, double *T, const DDTask &t, int tid, SY sync,
+                                          unsigned long long *mbg, unsigned par) {
+    const DDWalkPre wp = dd_walk_prefetch<0>(a, t.blk, t.tk, tid);  // in flight with the G copies
+    const double *G = a.gs + (t.task * a.n + t.r0) * (long long)DD_WMAX;
+    const bool bulk = (t.W & 1) == 0;
+    const int lane = tid & 31;
+    if (bulk && tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive_expect(mbg, (unsigned)(t.nrow * t.W * sizeof(double)));
+        for (int rl = 0; rl < t.nrow; ++rl)
+            bulk_g2s(T + cpad(rl) * DD_WPAD, G + (long long)rl * DD_WMAX, (unsigned)(t.W * sizeof(double)), mbg);
+    }
+    for (int rl = tid >> 5; rl < t.nrow; rl += DD2_THREADS / 32)
+#pragma unroll
+        for (int k = 0; k < (DD_WMAX + 31) / 32; ++k) {
+            const int ci = lane + 32 * k;
+            if (ci >= t.W && ci < DD_WMAX) T[cpad(rl) * DD_WPAD + ci] = 0.0;
+            else if (!bulk && ci < t.W) T[cpad(rl) * DD_WPAD + ci] = G[(long long)rl * DD_WMAX + ci];
+        }
+    if (bulk) mbar_wait(mbg, par);
+    sync();
+    dd_piece_walks<0>(a, T, t.blk, t.r0, t.nrow, t.tk, tid, wp);
+}
+// pass 2 after its GEMM: store with the fused epilogue; the tile is free again when this returns
+template <int DR, class SY>
+__device__ __forceinline__ void dd_p2_post(const DDStageArgs &a, double *T, const DDTask &t, int tid, SY sync) {
+    unsigned finm = 0;  // columns final after this stage (stage 1: all; stage 0: rho_1 = 0)
+    {
+        const double *rn_ot = a.rhon + (1 - a.stage) * a.n;
+        const int i0 = a.bi0[t.blk], lane = tid & 31;
+#pragma unroll
+        for (int k = 0; k < (DD_WMAX + 31) / 32; ++k) {
+            const int ci = lane + 32 * k;
+            if (ci < t.W && (a.stage == 1 || !(rn_ot[i0 + ci] > 0.0))) finm |= 1u << k;
+        }
+    }
+    dd_store_tile<DR, DD2_THREADS>(a, T, t.b, t.blk, t.r0, t.nrow, finm, tid);
+    sync();
+}
+
+// One tile per CTA, two CTAs per SM: one CTA's loads, walks and stores overlap the other's GEMM.
+template <int DR, int SRC, int PASS>
+__global__ void __launch_bounds__(DD2_THREADS, 2) dd_pass_kernel(DDStageArgs a) {
+    extern __shared__ double sh[];
+    double *T = sh;
+    __shared__ __align__(8) unsigned long long mbg;
+    const int tid = threadIdx.x;
+    const CtaSync sy{};
+    if (PASS == 2 && tid == 0) {
+        mbar_init(&mbg, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const DDTask t(a, blockIdx.x);
+    DD2T0;
+    if (PASS == 1) dd_p1_pre<DR, SRC>(a, T, t, tid, sy);
+    else dd_p2_pre(a, T, t, tid, sy, &mbg, 0);
+    DD2T(PASS == 1 ? 0 : 3);
+    const DDWalkPre wp = PASS == 1 ? dd_walk_prefetch<1>(a, t.blk, t.tk, tid) : DDWalkPre{};
+#ifdef PRS_DD_TIMING
+    if (!(a.abl & 1))
+#endif
+    dd_tile_gemm2(T, (PASS == 1 ? a.Q : a.QT)[t.blk], t.W, tid, sy);
+    DD2T(PASS == 1 ? 1 : 4);
+    if (PASS == 1) dd_p1_post(a, T, t, tid, sy, wp);
+    else dd_p2_post<DR>(a, T, t, tid, sy);
+    DD2T(PASS == 1 ? 2 : 5);
+#ifdef PRS_DD_TIMING
+    if (tid == 0) atomicAdd(&g_dd2_timing[PASS == 1 ? 7 : 8], 1ull);
+#endif
+}
+
+// per (state, block, mode): y_in of every sub-piece forward, then x_in backward
+__global__ void dd_scan_kernel(DDStageArgs a) {
+    const long long task = blockIdx.x;
+    const int am = threadIdx.x, W = a.bW[(int)(task % a.nblk)];
+    if (am >= W) return;
+    const int NS = 2 * a.CL;  // sub-pieces of the block
+    const long long s0 = task * NS;
+    constexpr int PB = 8;  // sub-pieces per batch: every load of a batch in flight together
+    double y = 0.0;
+    for (int p0 = 0; p0 < NS; p0 += PB) {
+        double tA[PB], tB[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            if (p0 + q < NS) {
+                const double *t = a.tup + (s0 + p0 + q) * 5 * DD_WMAX + am;
+                tA[q] = t[0];
+                tB[q] = t[DD_WMAX];
+            }
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            if (p0 + q < NS) {
+                a.bnd[(s0 + p0 + q) * 2 * DD_WMAX + am] = y;
+                y = fma(tA[q], y, tB[q]);
+            }
+    }
+    double x = 0.0;
+    for (int p1 = NS - 1; p1 >= 0; p1 -= PB) {
+        double tP[PB], t0[PB], t1[PB], yi[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            if (p1 - q >= 0) {
+                const double *t = a.tup + (s0 + p1 - q) * 5 * DD_WMAX + am;
+                tP[q] = t[2 * DD_WMAX];
+                t0[q] = t[3 * DD_WMAX];
+                t1[q] = t[4 * DD_WMAX];
+                yi[q] = a.bnd[(s0 + p1 - q) * 2 * DD_WMAX + am];
+            }
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            if (p1 - q >= 0) {
+                a.bnd[((s0 + p1 - q) * 2 + 1) * DD_WMAX + am] = x;
+                x = fma(tP[q], x, fma(t1[q], yi[q], t0[q]));
+            }
+    }
+}
+
 inline size_t dd_stage_smem_bytes() {
     // tile + two staged M chunks (the y-solve chunk maps alias them) + cluster totals
     static_assert(2 * DD_KC * DD_WPAD * sizeof(double) >= DD_NCH * DD_WMAX * sizeof(double2), "sc alias");
@@ -877,14 +1391,18 @@ struct DDData {
     // per tau slot (3) and colour (2): device arrays of per-block pointers + the storage
     double tau[3] = {-1.0, -1.0, -1.0};
     std::vector<double *> store[3];
-    const double **d_Q[3][2] = {}, **d_QT[3][2] = {}, **d_idy[3][2] = {};
+    const double **d_Q[3][2] = {}, **d_QT[3][2] = {}, **d_idy[3][2] = {}, **d_conv[3][2] = {};
     // global-exchange stage launch (default; PRS_DDCL=1: clusters)
     bool gx = true;
     int num_sms = 148;
     int *gbuf = nullptr;        // [1 + 2 * gcap]: task counter, flags
     double2 *gtot = nullptr;    // [gcap][2][DD_WMAX]
-    int gen = 0;                // bumped when gbuf / gtot are reallocated (captured graphs hold them)
+    int gen = 0;                // bumped when exchange / split scratch is reallocated (captured graphs hold it)
     long long gcap = 0;
+    // split stage (default; PRS_DDSPLIT=0: the single-kernel stage with the L2 exchange)
+    bool split = true;
+    double *gs = nullptr, *tup = nullptr, *bnd = nullptr;
+    long long scap = 0;         // block-states (B x blocks) the split scratch holds
     // full diffusion tensor (coef_kind 2, ddfull.cuh): d tables and per (slot, colour) the
     // block-Thomas factors E_l^T, P_l^{-1} of every block
     bool full = false;
@@ -976,6 +1494,8 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     }
     const char *clv = getenv("PRS_DDCL");
     d.gx = !(clv && clv[0] == '1');
+    const char *spv = getenv("PRS_DDSPLIT");
+    d.split = d.gx && !(spv && spv[0] == '0');
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1044,13 +1564,13 @@ inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
     }
     for (int col = 0; col < 2; ++col) {
         const size_t nb = d.bi0[col].size();
-        std::vector<const double *> hQ(nb), hQT(nb), hI(nb);
+        std::vector<const double *> hQ(nb), hQT(nb), hI(nb), hC(nb);
         for (size_t k = 0; k < nb; ++k) {
             const int W = d.bW[col][k];
             double *Q, *QT, *th, *idy;
             if (cudaMalloc(&Q, sizeof(double) * W * W) != cudaSuccess ||
                 cudaMalloc(&QT, sizeof(double) * W * W) != cudaSuccess ||
-                cudaMalloc(&th, sizeof(double) * W) != cudaSuccess ||
+                cudaMalloc(&th, sizeof(double) * 2 * W) != cudaSuccess ||
                 cudaMalloc(&idy, sizeof(double) * (size_t)W * d.n) != cudaSuccess) {
                 err = "cudaMalloc (DD factors) failed";
                 return PRS_ECUDA;
@@ -1062,21 +1582,25 @@ inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
             hQ[k] = Q;
             hQT[k] = QT;
             hI[k] = idy;
+            hC[k] = th + W;
         }
-        const double **dq, **dqt, **di;
+        const double **dq, **dqt, **di, **dc;
         if (cudaMalloc(&dq, sizeof(double *) * nb) != cudaSuccess ||
             cudaMalloc(&dqt, sizeof(double *) * nb) != cudaSuccess ||
-            cudaMalloc(&di, sizeof(double *) * nb) != cudaSuccess) {
+            cudaMalloc(&di, sizeof(double *) * nb) != cudaSuccess ||
+            cudaMalloc(&dc, sizeof(double *) * nb) != cudaSuccess) {
             err = "cudaMalloc (DD pointer tables) failed";
             return PRS_ECUDA;
         }
-        d.store[slot].insert(d.store[slot].end(), {(double *)dq, (double *)dqt, (double *)di});
+        d.store[slot].insert(d.store[slot].end(), {(double *)dq, (double *)dqt, (double *)di, (double *)dc});
         cudaMemcpyAsync(dq, hQ.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(dqt, hQT.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(di, hI.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(dc, hC.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
         d.d_Q[slot][col] = dq;
         d.d_QT[slot][col] = dqt;
         d.d_idy[slot][col] = di;
+        d.d_conv[slot][col] = dc;
     }
     if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
         err = "DD factorisation failed";
@@ -1092,7 +1616,7 @@ inline void dd_free(DDData &d) {
     }
     if (d.gbuf) cudaFree(d.gbuf);
     if (d.gtot) cudaFree(d.gtot);
-    double *bufs[] = {d.rhon, d.rhof, d.Z, d.dxf, d.dyf};
+    double *bufs[] = {d.rhon, d.rhof, d.Z, d.dxf, d.dyf, d.gs, d.tup, d.bnd};
     for (double *p : bufs)
         if (p) cudaFree(p);
     for (int c = 0; c < 2; ++c) {
@@ -1174,6 +1698,10 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
         a.Q = d.d_Q[slot][stage];
         a.QT = d.d_QT[slot][stage];
         a.idy = d.d_idy[slot][stage];
+        a.conv = d.d_conv[slot][stage];
+#ifdef PRS_DD_TIMING
+        a.abl = getenv("PRS_DD_ABL") ? atoi(getenv("PRS_DD_ABL")) : 0;
+#endif
         a.tau = d.tau[slot];
         a.h2inv = d.h2inv;
         a.c = d.c;
@@ -1189,6 +1717,67 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
         a.e_traj = traj;
         a.e_red = red;
         const long long ntasks = B * a.nblk * CL;
+        if (d.split) {
+            if (B * a.nblk > d.scap) {
+                double *bufs[] = {d.gs, d.tup, d.bnd};
+                for (double *p : bufs)
+                    if (p) cudaFree(p);
+                d.gs = d.tup = d.bnd = nullptr;
+                d.scap = 0;
+                if (cudaMalloc(&d.gs, sizeof(double) * DD_WMAX * (size_t)n * B * a.nblk) != cudaSuccess ||
+                    cudaMalloc(&d.tup, sizeof(double) * 5 * DD_WMAX * 2 * ntasks) != cudaSuccess ||
+                    cudaMalloc(&d.bnd, sizeof(double) * 2 * DD_WMAX * 2 * ntasks) != cudaSuccess) {
+                    err = "cudaMalloc (DD split scratch) failed";
+                    return PRS_ECUDA;
+                }
+                d.scap = B * a.nblk;
+                ++d.gen;
+            }
+            a.gs = d.gs;
+            a.tup = d.tup;
+            a.bnd = d.bnd;
+            a.ntasks = (int)ntasks;
+            void (*k1)(DDStageArgs) = nullptr, (*k2)(DDStageArgs) = nullptr;
+            const int dr = scheme == PRS_DR;
+#define DK(D, S_)                     \
+    if (dr == D && src == S_) {       \
+        k1 = dd_pass_kernel<D, S_, 1>; \
+        k2 = dd_pass_kernel<D, S_, 2>; \
+    }
+            DK(0, 0) DK(0, 1) DK(1, 0) DK(1, 1)
+#undef DK
+            const size_t shm2 = sizeof(double) * (size_t)(cpad(DD_RMAX - 1) + 1) * DD_WPAD;  // the tile only
+            if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm2) != cudaSuccess ||
+                cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm2) != cudaSuccess) {
+                err = "cudaFuncSetAttribute(dd split passes) failed";
+                return PRS_ECUDA;
+            }
+            const unsigned nthr = DD2_THREADS, grid = (unsigned)ntasks;
+            if (prof && prs_internal_prof_begin(prof) != PRS_OK) return PRS_ECUDA;
+            void (*ks[3])(DDStageArgs) = {k1, dd_scan_kernel, k2};
+            for (int q = 0; q < 3; ++q) {
+                if (q == 1) dd_scan_kernel<<<(unsigned)(B * a.nblk), DD_WMAX, 0, st>>>(a);
+                else ks[q]<<<grid, nthr, shm2, st>>>(a);
+                launches++;
+                const cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) {
+                    cudaFuncAttributes fa{};
+                    cudaFuncGetAttributes(&fa, ks[q]);
+                    err = std::string("dd split stage, launch ") + std::to_string(q) + ": " + cudaGetErrorString(e) +
+                          " (regs " + std::to_string(fa.numRegs) + ", max threads " +
+                          std::to_string(fa.maxThreadsPerBlock) + ", static smem " + std::to_string(fa.sharedSizeBytes) +
+                          ", dynamic " + std::to_string(q == 1 ? 0 : shm2) + ", threads " +
+                          std::to_string(q == 1 ? DD_WMAX : (int)nthr) + ")";
+                    return PRS_ECUDA;
+                }
+            }
+            if (prof) {
+                double flops = 0.0;
+                for (int w : d.bW[stage]) flops += (double)w * n * (4.0 * w + 10.0);
+                if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
+            }
+            continue;
+        }
         if (d.gx && ntasks > d.gcap) {
             if (d.gbuf) cudaFree(d.gbuf);
             if (d.gtot) cudaFree(d.gtot);

@@ -1065,6 +1065,14 @@ void prs_destroy(prs_ctx *ctx) {
         if (h[3])
             fprintf(stderr, "DD timing: %llu tasks, per task %.1f us, forward wait %.1f us, backward wait %.1f us\n",
                     h[3], h[2] / 1e3 / h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3]);
+        unsigned long long g[9];
+        cudaMemcpyFromSymbol(g, prs::g_dd2_timing, sizeof(g));
+        if (g[7] && g[8])
+            fprintf(stderr,
+                    "DD split timing (us per task, thread 0): p1 %llu tasks: load %.2f gemm(+turn) %.2f store+walk %.2f "
+                    "| p2 %llu tasks: load+walk %.2f gemm(+turn) %.2f store %.2f\n",
+                    g[7], g[0] / 1e3 / g[7], g[1] / 1e3 / g[7], g[2] / 1e3 / g[7], g[8], g[3] / 1e3 / g[8],
+                    g[4] / 1e3 / g[8], g[5] / 1e3 / g[8]);
     }
 #endif
 #ifdef PRS_X7_TIMING

@@ -177,14 +177,17 @@ DD_STEP_CASES = [
 ]
 
 
-@pytest.mark.parametrize("exchange", ["l2", "cluster"])
+@pytest.mark.parametrize("exchange", ["split", "l2", "cluster"])
 @pytest.mark.parametrize("p", DD_STEP_CASES, ids=lambda p: f"n{p.n}_S{p.dd_strips}_b{p.dd_overlap}_r{p.dd_ramp}")
 def test_dd_single_step_parity(p, exchange, monkeypatch):
     """DD stage solves (separable eigen-transform + row-piece tridiagonal) vs the oracle's band
-    elimination, FIE and DR, small and large tau; row pieces exchanging their scan totals
-    through L2 (default, persistent grid) or within a cluster (PRS_DDCL=1)."""
+    elimination, FIE and DR, small and large tau; the row pieces of a block as independent
+    passes with a scan of their transfer tuples between them (default), or exchanging scan
+    totals through L2 in one persistent kernel (PRS_DDSPLIT=0) or within a cluster (PRS_DDCL=1)."""
     if exchange == "cluster":
         monkeypatch.setenv("PRS_DDCL", "1")
+    elif exchange == "l2":
+        monkeypatch.setenv("PRS_DDSPLIT", "0")
     prs = prs_mod()
     ctx = prs.Context(p)
     o = oracle.Oracle(p)
