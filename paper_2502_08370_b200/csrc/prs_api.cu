@@ -132,6 +132,9 @@ struct TauFactors {
 };
 
 struct prs_ctx {
+    bool x7_tma = true;        // c3 x pass: TMA tensor copies (PRS_X7TMA=0: cp.async + staged stores)
+    // TMA tensor maps (rows of 16 doubles, 128-byte swizzle) by (address, rows)
+    std::vector<std::pair<std::pair<const void *, long long>, CUtensorMap>> tmaps;
     prs_problem p{};
     int rank = 0, nranks = 1, first = 0, count = 0;
     // slice ownership (prs_set_ownership): 0 contiguous blocks (local slice i = global first + i;
@@ -391,6 +394,47 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     return PRS_OK;
 }
 
+// ---- TMA tensor maps: a buffer of `rows` x 16 doubles (128-byte rows), box 16 x 128 (a half
+// row of xpass7), 128-byte swizzle; encoded through the driver entry point (no link-time libcuda
+// dependency) and cached per (address, rows)
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int get_tmap(prs_ctx *ctx, const void *ptr, long long rows, CUtensorMap *out) {
+    for (auto &e : ctx->tmaps)
+        if (e.first.first == ptr && e.first.second == rows) {
+            *out = e.second;
+            return PRS_OK;
+        }
+    static PFN_encodeTiled encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) {
+            ctx->err = "cuTensorMapEncodeTiled unavailable";
+            return PRS_ECUDA;
+        }
+        encode = reinterpret_cast<PFN_encodeTiled>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)LCH, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(LCH * sizeof(double))};
+    const cuuint32_t box[2] = {(cuuint32_t)LCH, (cuuint32_t)X7T};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptr), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        ctx->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+        return PRS_ECUDA;
+    }
+    if (ctx->tmaps.size() > 64) ctx->tmaps.clear();
+    ctx->tmaps.push_back({{ptr, rows}, m});
+    *out = m;
+    return PRS_OK;
+}
+
 // 4096-point rows (c3): each row over a 2-CTA cluster (xpass7.cuh)
 static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out, long long B,
                          const TimeArgs &ta, bool prof) {
@@ -422,11 +466,19 @@ static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.s2n = ctx->s2n;
     a.s2f = ctx->s2f;
     const int dr = (scheme == PRS_DR) ? 1 : 0, coef = ctx->p.coef_kind, src = ctx->p.source_kind;
+    const int tma = ctx->x7_tma ? 1 : 0;
+    if (tma) {
+        TRY(get_tmap(ctx, in, B * ctx->vol / LCH, &a.tm_in));
+        TRY(get_tmap(ctx, out, B * ctx->vol / LCH, &a.tm_out));
+        if (coef) TRY(get_tmap(ctx, f.invdx, ctx->vol / LCH, &a.tm_piv));
+    }
     void (*kern)(X7Args) = nullptr;
-#define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass7_kernel<C, D, S_>;
+#define XK(C, D, S_)                                                  \
+    if (coef == C && dr == D && src == S_)                            \
+        kern = tma ? xpass7_kernel<C, D, S_, 1> : xpass7_kernel<C, D, S_, 0>;
     XK(0, 0, 0) XK(0, 0, 1) XK(0, 1, 0) XK(0, 1, 1) XK(1, 0, 0) XK(1, 0, 1) XK(1, 1, 0) XK(1, 1, 1)
 #undef XK
-    const size_t shm = xpass7_smem_bytes(coef);
+    const size_t shm = xpass7_smem_bytes(coef, tma);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * std::min<long long>(ncl, a.nrows)));
@@ -933,6 +985,8 @@ static int create_impl(const prs_problem *prob, int rank, int nranks, Transport 
         ctx->lag = !(lg && lg[0] == '0');
         const char *gv = getenv("PRS_GRAPHS");
         ctx->graphs = !(gv && gv[0] == '0');
+        const char *tv = getenv("PRS_X7TMA");
+        ctx->x7_tma = !(tv && tv[0] == '0');
     }
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;

@@ -13,7 +13,18 @@
 //             CTA 1's half, right after CTA 0's first walk and scan;
 //   backward: CTA 1's x at its first point (its backward maps composed from x = 0 at the row
 //             end, after its exact forward recurrence), to CTA 0 before CTA 0's last walk.
+//
+// TMA = 1 (default): the ring slots are filled by TMA tensor copies (one 2-D copy of 128 rows of
+// 128 bytes per half row, issued by one thread, completing on the slot's mbarrier) and the
+// output half row leaves by one TMA tensor store from a staging slot; the tensor maps' 128-byte
+// swizzle puts 16-byte unit u of chunk k at unit u ^ (k & 7), so the per-thread chunk accesses
+// stay bank-conflict free without padding.  No per-thread copy instructions remain for the
+// 48 KB a row moves through shared memory (TMA = 0: 16-byte cp.async fills, staged coalesced
+// stores; the load/store issue ahead of each row cost ~1k cycles of its chain,
+// profiles/r02_notes.md).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 #include "xpass3.cuh"
 
@@ -42,6 +53,7 @@ constexpr int X7G = X7T * X3C;     // doubles per half-row slot (padded chunk la
 constexpr int X7N = 2 * X7T * LCH; // row length (4096)
 
 struct X7Args {
+    CUtensorMap tm_in, tm_out, tm_piv;  // TMA: the batch in / out and the x pivots as rows of 16 doubles
     const double *in;
     double *out;
     long long vol;        // slice stride (= n^2)
@@ -55,14 +67,24 @@ struct X7Args {
     const double *invd, *s2n, *s2f;
 };
 
-inline size_t xpass7_smem_bytes(int coef) { return sizeof(double) * ((size_t)(4 + (coef ? 2 : 1)) * X7G) + 8 * 16; }
+constexpr int X7S = X7T * LCH;      // doubles per half-row slot (TMA: unpadded, swizzled)
+inline size_t xpass7_smem_bytes(int coef, int tma) {
+    if (tma) return sizeof(double) * ((size_t)6 * X7S) + 1024 + 8 * 16;
+    return sizeof(double) * ((size_t)(4 + (coef ? 2 : 1)) * X7G) + 8 * 16;
+}
 
-template <int COEF, int DR, int SRC>
-__global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
-    extern __shared__ __align__(16) double smem[];
+template <int COEF, int DR, int SRC, int TMA>
+__global__ void __launch_bounds__(X7T, 2) xpass7_kernel(const __grid_constant__ X7Args a) {
+    extern __shared__ __align__(16) double smem_raw[];
+    // TMA: slots 1024-byte aligned (the 128-byte swizzle atom)
+    double *smem = TMA ? reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023)
+                       : smem_raw;
+    constexpr int SLOT = TMA ? X7S : X7G;  // doubles per slot
     double *ubuf = smem;                     // 4 half-row state slots
-    double *ibuf = smem + 4 * X7G;           // COEF: 2 pivot slots; else 1 output staging slot
-    double2 *scr = reinterpret_cast<double2 *>(smem + (4 + (COEF ? 2 : 1)) * X7G);  // [4] fwd, [4] bwd
+    double *ibuf = smem + 4 * SLOT;          // 2 pivot slots (COEF; the output staging after the walks),
+                                             // else 1 staging slot (TMA: 2)
+    double2 *scr = reinterpret_cast<double2 *>(smem + (4 + ((COEF || TMA) ? 2 : 1)) * SLOT);  // [4] fwd, [4] bwd
+    __shared__ __align__(8) unsigned long long mbu[4], mbp[2];  // TMA: one per ring slot
     __shared__ __align__(16) double2 xin;    // message from the partner CTA
     __shared__ __align__(8) unsigned long long mbx;
     cg::cluster_group cl = cg::this_cluster();
@@ -74,6 +96,10 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
 
     if (k == 0) {
         mbar_init(&mbx, 1);
+        if (TMA) {
+            for (int i = 0; i < 4; ++i) mbar_init(mbu + i, 1);
+            for (int i = 0; i < 2; ++i) mbar_init(mbp + i, 1);
+        }
         mbar_fence_init();
     }
     // ---- per-thread x-dependent data ----
@@ -101,6 +127,8 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
     long long tlast = clock64();
 #endif
 
+    // offset (doubles) of 16-byte unit u of chunk c within a slot
+    auto uoff = [&](int c, int u) { return TMA ? c * LCH + ((u ^ (c & 7)) << 1) : c * X3C + 2 * u; };
     auto issue_group = [&](const double *rowp, double *dst) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -109,10 +137,42 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             cp_async16(dst + c * X3C + 2 * u, rowp + hoff + 2 * p);
         }
     };
-    auto ub = [&](long long g) { return ubuf + (int)(g & 3) * X7G; };
-    auto ib = [&](long long g) { return ibuf + (COEF ? (int)(g & 1) : 0) * X7G; };
-    auto issue_state = [&](long long g) { issue_group(a.in + (g >> 12) * a.vol + (g & 4095) * (long long)n, ub(g)); };
-    auto issue_piv = [&](long long g) { issue_group(a.invd + (g & 4095) * (long long)n, ib(g)); };
+    auto ub = [&](long long g) { return ubuf + (int)(g & 3) * SLOT; };
+    auto ib = [&](long long g) { return ibuf + ((COEF || TMA) ? (int)(g & 1) : 0) * SLOT; };
+    // TMA: tensor row (128-byte row = chunk) of this CTA's half of batch row g / pivot row j
+    auto trow_state = [&](long long g) { return (g >> 12) * (a.vol / LCH) + (g & 4095) * (X7N / LCH) + crank * X7T; };
+    auto tma_load = [&](const CUtensorMap *tm, long long tr, double *dst, unsigned long long *mb) {
+        mbar_arrive_expect(mb, (unsigned)(X7S * sizeof(double)));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+                "r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"((int)tr), "r"(smem_u32(mb))
+            : "memory");
+    };
+    auto issue_state = [&](long long g) {
+        if (TMA) {
+            if (k == 0) tma_load(&a.tm_in, trow_state(g), ub(g), mbu + (g & 3));
+        } else {
+            issue_group(a.in + (g >> 12) * a.vol + (g & 4095) * (long long)n, ub(g));
+        }
+    };
+    auto issue_piv = [&](long long g) {
+        if (TMA) {
+            if (k == 0) tma_load(&a.tm_piv, (g & 4095) * (X7N / LCH) + crank * X7T, ib(g), mbp + (g & 1));
+        } else {
+            issue_group(a.invd + (g & 4095) * (long long)n, ib(g));
+        }
+    };
+    // TMA: every thread waits once on every fill, in issue order; bits = parity of each slot's next fill
+    unsigned upar = 0, ppar = 0;
+    long long wr = 0, wlast = -1;  // next state row to wait for, last row issued in this task
+    auto wait_rows = [&](long long upto) {
+        for (; wr <= upto && wr <= wlast; ++wr) {
+            const int sl = (int)(wr & 3);
+            mbar_wait(mbu + sl, (upar >> sl) & 1u);
+            upar ^= 1u << sl;
+        }
+    };
 
     struct LineScalars {
         double kfm, kfp, hsx, srcf, idm1;
@@ -147,48 +207,66 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             g1 = g0 + per + (task < rem ? 1 : 0);
         }
         __syncthreads();
+        if (TMA && k == 0) {
+            // the slots were last read by generic loads (and the staging slots by TMA stores)
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        }
         if (g0 < g1) {
+            wr = (DR && g0 > 0) ? g0 - 1 : g0;
+            wlast = min(G - 1, g1 - 1 + (DR ? 1 : 0));
             if (DR && g0 > 0) issue_state(g0 - 1);
             issue_state(g0);
             if (COEF) issue_piv(g0);
             cp_async_commit();
-            if (g0 + 1 < G) issue_state(g0 + 1);
+            if (g0 + 1 <= wlast) issue_state(g0 + 1);
             cp_async_commit();
         }
         LineScalars nxt = line_scalars(g0);
         for (long long g = g0; g < g1; ++g) {
             const LineScalars cur = nxt;
             nxt = line_scalars(g + 1);
+            // every generic access of the slots refilled below is behind the last barrier
+            if (TMA && k == 0 && g > g0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             if (g + 2 < G && g + 2 < g1 + (DR ? 1 : 0)) issue_state(g + 2);
-            if (COEF && g + 1 < g1) issue_piv(g + 1);
-            cp_async_commit();
+            // (TMA: the pivots of row g + 1 go into the staging slot of row g - 1, after its store
+            // has read it out -- issued after this row's first walk, below)
+            if (!TMA && COEF && g + 1 < g1) issue_piv(g + 1);
+            if (!TMA) cp_async_commit();
             X7T_MARK(8);  // scalars + issue
-            cp_async_wait<1>();
+            if (TMA) {
+                wait_rows(g + (DR ? 1 : 0));
+                if (COEF) {
+                    mbar_wait(mbp + (g & 1), (ppar >> (g & 1)) & 1u);
+                    ppar ^= 1u << (g & 1);
+                }
+            } else {
+                cp_async_wait<1>();
+            }
             if (k == 0) mbar_arrive_expect(&mbx, 16);  // this row's incoming message
-            X7T_MARK(0);  // cp.async wait for this row's group
-            __syncthreads();
-            X7T_MARK(1);  // wait for this row's data
+            X7T_MARK(0);  // wait for this row's copies
+            if (!TMA) __syncthreads();
+            X7T_MARK(1);  // barrier (cp.async: every thread's copies visible)
 
             const int j = (int)(g & 4095);
             const double *U = ub(g);
             double v[LCH], w[LCH];
             {
-                const double *src = U + k * X3C;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const double2 x = *reinterpret_cast<const double2 *>(src + 2 * u);
+                    const double2 x = *reinterpret_cast<const double2 *>(U + uoff(k, u));
                     v[2 * u] = x.x;
                     v[2 * u + 1] = x.y;
                 }
             }
             if (DR) {  // w = tau A_y U (rows j -+ 1 of the same half, from the ring)
                 const bool hm = j > 0, hp = j < n - 1;
-                const double *um = ub(g - 1) + k * X3C, *up = ub(g + 1) + k * X3C;
+                const double *um = ub(g - 1), *up = ub(g + 1);
                 const double kfm = 0.5 * cur.kfm, kfp = 0.5 * cur.kfp;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const double2 xm = hm ? *reinterpret_cast<const double2 *>(um + 2 * u) : make_double2(0.0, 0.0);
-                    const double2 xp = hp ? *reinterpret_cast<const double2 *>(up + 2 * u) : make_double2(0.0, 0.0);
+                    const double2 xm = hm ? *reinterpret_cast<const double2 *>(um + uoff(k, u)) : make_double2(0.0, 0.0);
+                    const double2 xp = hp ? *reinterpret_cast<const double2 *>(up + uoff(k, u)) : make_double2(0.0, 0.0);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int i = 2 * u + h;
@@ -207,14 +285,14 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             }
             double idr[LCH], idm1 = 0.0, hsx = 0.0;
             if (COEF) {
-                const double *I = ib(g) + k * X3C;
+                const double *I = ib(g);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const double2 x = *reinterpret_cast<const double2 *>(I + 2 * u);
+                    const double2 x = *reinterpret_cast<const double2 *>(I + uoff(k, u));
                     idr[2 * u] = x.x;
                     idr[2 * u + 1] = x.y;
                 }
-                idm1 = (k > 0) ? I[-X3C + LCH - 1] : cur.idm1;
+                idm1 = (k > 0) ? I[uoff(k - 1, 7) + 1] : cur.idm1;
                 hsx = 0.5 * cur.hsx;
             }
             X7T_MARK(2);  // loads + DR stencil
@@ -235,6 +313,15 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
             if (lane == 31) scr[warp] = make_double2(A, B);
             __syncthreads();
             X7T_MARK(3);  // F1 + forward warp scan + barrier
+            if (TMA && k == 0) {
+                // the staging slot of row g - 1 (its store has read it out by now) takes the
+                // pivots of row g + 1 (COEF), or row g + 1's output (barriers before it is written)
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                if (COEF && g + 1 < g1) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    issue_piv(g + 1);
+                }
+            }
             double Yc = 0.0;  // y entering this CTA's half
             if (crank == 0) {
                 if (k == 0) {  // y at the end of the half from y = 0 at the row start -> CTA 1
@@ -301,6 +388,31 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
                 x = fma(cid(i), v[i], -ccc(i) * x);
                 v[i] = DR ? x - w[i] : x;
             }
+#ifdef PRS_X7_DIRECT
+            {  // experiment: each thread stores its chunk (one 128-byte line) straight from registers
+                double *o = a.out + (g >> 12) * a.vol + (long long)j * n + hoff + (long long)k * LCH;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    *reinterpret_cast<double2 *>(o + 2 * u) = make_double2(v[2 * u], v[2 * u + 1]);
+            }
+            __syncthreads();  // every read of ib(g), scr and xin is done before the slots are refilled
+#else
+            if (TMA) {
+                __syncthreads();  // every read of ib(g), scr and xin is done
+                double *dst = ib(g);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    *reinterpret_cast<double2 *>(dst + uoff(k, u)) = make_double2(v[2 * u], v[2 * u + 1]);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA reads
+                __syncthreads();
+                if (k == 0) {
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                                     reinterpret_cast<uint64_t>(&a.tm_out)),
+                                 "r"(0), "r"((int)trow_state(g)), "r"(smem_u32(dst))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                }
+            } else {
             __syncthreads();  // every read of ib(g), scr and xin is done
             {
                 double *dst = ib(g) + k * X3C;
@@ -321,13 +433,16 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(X7Args a) {
                 }
             }
             __syncthreads();  // staging slot free before the next prefetch lands in it
+            }
+#endif
             X7T_MARK(7);  // B3 + staging + store
 #ifdef PRS_X7_TIMING
             if (k == 0) tacc[9] += 1;
 #endif
         }
-        cp_async_wait<0>();
+        if (!TMA) cp_async_wait<0>();
     }
+    if (TMA && k == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores done
 #ifdef PRS_X7_TIMING
     if (k == 0)
         for (int p = 0; p < 10; ++p) atomicAdd(&g_x7_timing[crank][p], tacc[p]);
