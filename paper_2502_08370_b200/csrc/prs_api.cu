@@ -132,6 +132,7 @@ struct TauFactors {
 };
 
 struct prs_ctx {
+    double *cyc2 = nullptr;    // cyclic ownership, on-chip chain: two-state scratch (chain2_cyclic_one)
     bool x7_tma = true;        // c3 x pass: TMA tensor copies (PRS_X7TMA=0: cp.async + staged stores)
     // TMA tensor maps (rows of 16 doubles, 128-byte swizzle) by (address, rows)
     std::vector<std::pair<std::pair<const void *, long long>, CUtensorMap>> tmaps;
@@ -1146,7 +1147,7 @@ void prs_destroy(prs_ctx *ctx) {
     }
 #endif
     delete ctx->tr;
-    double *bufs[] = {ctx->traj, ctx->fa, ctx->fb, ctx->gcache, ctx->gtmp, ctx->u0,
+    double *bufs[] = {ctx->traj, ctx->fa, ctx->fb, ctx->gcache, ctx->gtmp, ctx->u0, ctx->cyc2,
                       ctx->sinpi, ctx->s2n, ctx->s2f, ctx->tend};
     for (double *b : bufs)
         if (b) cudaFree(b);
@@ -1202,6 +1203,7 @@ int prs_set_initial(prs_ctx *ctx, const double *u0, int u0_on_device) {
 
 static bool sweep2_ok(const prs_ctx *ctx);
 static int launch_chain2(prs_ctx *ctx, int i0, int epi);
+static int chain2_cyclic_one(prs_ctx *ctx, int i, int epi);
 
 static TimeArgs coarse_time(prs_ctx *ctx, int slice) {
     TimeArgs ta;
@@ -1222,12 +1224,16 @@ int prs_coarse_sweep(prs_ctx *ctx) {
         for (int i = 0; i < ctx->count; ++i) {
             const int n = (int)gslice(ctx, i);
             if (n > 0) NK(ctx->tr->recv(state(ctx, ctx->traj, i), (size_t)ctx->vol, owner_of(ctx, n - 1), ctx->stream));
-            EpiArgs ep;
-            ep.kind = EPI_INIT;
-            ep.gcache = state(ctx, ctx->gcache, i);
-            ep.traj = end_state(ctx, i);
-            TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1, coarse_time(ctx, n), ep,
-                         false, ctx->ss));
+            if (sweep2_ok(ctx)) {
+                TRY(chain2_cyclic_one(ctx, i, EPI_INIT));
+            } else {
+                EpiArgs ep;
+                ep.kind = EPI_INIT;
+                ep.gcache = state(ctx, ctx->gcache, i);
+                ep.traj = end_state(ctx, i);
+                TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1, coarse_time(ctx, n),
+                             ep, false, ctx->ss));
+            }
             if (n + 1 < ctx->p.N)
                 NK(ctx->tr->send(end_state(ctx, i), (size_t)ctx->vol, owner_of(ctx, n + 1), ctx->stream));
         }
@@ -1326,7 +1332,8 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
 // the coarse chain of local slices i0 .. i1-1 on chip (sweep2 with CHAIN = 1): one cluster.
 // traj / gcache / delta are batch buffers (slice stride ss); U_{i0} is read from traj.
 static int launch_chain2x(prs_ctx *ctx, double *traj, double *gcache, const double *delta, int i0, int i1, int epi,
-                          unsigned long long *red, cudaStream_t st, const double *trajold = nullptr) {
+                          unsigned long long *red, cudaStream_t st, const double *trajold = nullptr,
+                          long long slice0 = -1) {
     const int n = ctx->p.n, cnt = i1 - i0;
     if (cnt <= 0) return PRS_OK;
     const TauFactors &f = ctx->fac[0];
@@ -1344,7 +1351,7 @@ static int launch_chain2x(prs_ctx *ctx, double *traj, double *gcache, const doub
     a.creact = ctx->creact;
     a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
     a.sinpi = ctx->sinpi;
-    a.slice0 = ctx->first + i0;
+    a.slice0 = slice0 >= 0 ? slice0 : ctx->first + i0;
     a.sstride = 1;
     a.dt = ctx->dT;
     a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
@@ -1386,6 +1393,21 @@ static int launch_chain2x(prs_ctx *ctx, double *traj, double *gcache, const doub
 
 static int launch_chain2(prs_ctx *ctx, int i0, int epi) {
     return launch_chain2x(ctx, ctx->traj, ctx->gcache, ctx->delta, i0, ctx->count, epi, ctx->red, ctx->stream);
+}
+
+// cyclic ownership, on-chip shapes: the G step (+ epilogue) of local slice i by the same on-chip
+// chain kernel as contiguous ownership (so the results stay bitwise those of one rank): the chain
+// runs on a two-state scratch [U_i, U_{i+1}]; U_{i+1} (and, for the update norm, the old end
+// state) live in tend[i]
+static int chain2_cyclic_one(prs_ctx *ctx, int i, int epi) {
+    if (!ctx->cyc2) CK(cudaMalloc(&ctx->cyc2, sizeof(double) * 2 * ctx->ss));
+    double *te = const_cast<double *>(end_state(ctx, i));
+    CK(cudaMemcpyAsync(ctx->cyc2, state(ctx, ctx->traj, i), sizeof(double) * ctx->vol, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    TRY(launch_chain2x(ctx, ctx->cyc2, state(ctx, ctx->gcache, i), epi == EPI_CORRECT ? state(ctx, ctx->delta, i) : nullptr,
+                       0, 1, epi, ctx->red, ctx->stream, epi == EPI_CORRECT ? te - ctx->ss : nullptr, gslice(ctx, i)));
+    CK(cudaMemcpyAsync(te, ctx->cyc2 + ctx->ss, sizeof(double) * ctx->vol, cudaMemcpyDeviceToDevice, ctx->stream));
+    return PRS_OK;
 }
 
 static int enqueue_fine_sweep(prs_ctx *ctx) {
@@ -1729,13 +1751,17 @@ static int enqueue_chain_mr(prs_ctx *ctx) {
             const int n = (int)gslice(ctx, i);
             if (n > ctx->kconv)
                 NK(ctx->tr->recv(state(ctx, ctx->traj, i), (size_t)ctx->vol, owner_of(ctx, n - 1), ctx->stream));
-            EpiArgs ep;
-            ep.kind = EPI_CORRECT;
-            ep.gcache = state(ctx, ctx->gcache, i);
-            ep.delta = state(ctx, ctx->delta, i);
-            ep.traj = end_state(ctx, i);
-            TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1, coarse_time(ctx, n), ep,
-                         false, ctx->ss));
+            if (sweep2_ok(ctx)) {
+                TRY(chain2_cyclic_one(ctx, i, EPI_CORRECT));
+            } else {
+                EpiArgs ep;
+                ep.kind = EPI_CORRECT;
+                ep.gcache = state(ctx, ctx->gcache, i);
+                ep.delta = state(ctx, ctx->delta, i);
+                ep.traj = end_state(ctx, i);
+                TRY(run_step(ctx, ctx->p.G, ctx->fac[0], state(ctx, ctx->traj, i), ctx->gtmp, 1, coarse_time(ctx, n),
+                             ep, false, ctx->ss));
+            }
             if (n + 1 < ctx->p.N)
                 NK(ctx->tr->send(end_state(ctx, i), (size_t)ctx->vol, owner_of(ctx, n + 1), ctx->stream));
         }
