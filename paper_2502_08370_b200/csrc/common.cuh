@@ -211,6 +211,14 @@ __device__ __forceinline__ void st_async_remote_f64(double *dst, unsigned long l
                  : "memory");
 }
 
+// fp64 tensor-core MMA (m8n8k4, row.col): D = A B + C on an 8 x 8 tile; per lane A[lane / 4][lane % 4],
+// B[lane % 4][lane / 4], C / D [lane / 4][2 (lane % 4) + 0, 1]
+__device__ __forceinline__ void dmma_f64(double &c0, double &c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
 // Walk dispatch: `full` must be uniform over the CTA (every chunk of every line has LCH
 // elements, or the predicated variant runs).
 template <class V>

@@ -40,6 +40,7 @@
 #include "../../include/prs.h"
 #include "common.cuh"
 #include "ddfull.cuh"
+#include "dfpart.cuh"
 #include "lpass.cuh"
 #include "xpass3.cuh"
 
@@ -340,11 +341,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
-__device__ __forceinline__ void dmma_f64(double &c0, double &c1, double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(c0), "+d"(c1)
-        : "d"(a), "d"(b));
-}
 __device__ __forceinline__ void dd_tile_gemm(double *T, const double *M, int W, int nrow, double *Ms) {
     // fp64 tensor-core MMA (m8n8k4): warp w owns rows 16 (w % NCH) .. +15 and columns
     // 72 (w / NCH) .. +71 of the output, i.e. 2 x 9 tiles of 8 x 8, accumulators in registers.
@@ -1409,6 +1405,12 @@ struct DDData {
     double h = 0;
     double *dxf = nullptr, *dyf = nullptr;
     double **d_ET[3][2] = {}, **d_PI[3][2] = {};
+    // partitioned application (dfpart.cuh, default; PRS_DFPART=0: df_stage_kernel): per (slot,
+    // colour) A_p^T, Pp_p^T of every block; scratch tiles sized for dcap block-groups
+    bool dfpart = true;
+    double **d_AT[3][2] = {}, **d_PpT[3][2] = {};
+    double *dfp_tl = nullptr, *dfp_by = nullptr, *dfp_bx = nullptr, *dfp_ys = nullptr;
+    long long dcap = 0;
 };
 
 inline DFOp df_op(const DDData &d, int colour) {
@@ -1496,6 +1498,8 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     d.gx = !(clv && clv[0] == '1');
     const char *spv = getenv("PRS_DDSPLIT");
     d.split = d.gx && !(spv && spv[0] == '0');
+    const char *dpv = getenv("PRS_DFPART");
+    d.dfpart = !(dpv && dpv[0] == '0');
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1541,6 +1545,51 @@ inline int df_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
         }
         df_factor_kernel<<<(unsigned)nb, DF_FTHREADS, fsm, st>>>(df_op(d, col), d.d_bi0[col], d.d_bW[col], tau, dE,
                                                                dP);
+        if (d.dfpart) {
+            // the partition products A_p^T, Pp_p^T: the sweeps of dfpart.cuh on unit columns
+            const int P = (d.n + DFP_M - 1) / DFP_M;
+            std::vector<double *> hA(nb), hPp(nb);
+            for (size_t k = 0; k < nb; ++k) {
+                const size_t bytes = sizeof(double) * (size_t)P * d.bW[col][k] * d.bW[col][k];
+                if (cudaMalloc(&hA[k], bytes) != cudaSuccess || cudaMalloc(&hPp[k], bytes) != cudaSuccess) {
+                    err = "cudaMalloc (full-tensor partition products) failed";
+                    return PRS_ECUDA;
+                }
+                d.store[slot].insert(d.store[slot].end(), {hA[k], hPp[k]});
+            }
+            double **dA, **dPp;
+            if (cudaMalloc(&dA, sizeof(double *) * nb) != cudaSuccess ||
+                cudaMalloc(&dPp, sizeof(double *) * nb) != cudaSuccess) {
+                err = "cudaMalloc (full-tensor pointer tables) failed";
+                return PRS_ECUDA;
+            }
+            d.store[slot].insert(d.store[slot].end(), {(double *)dA, (double *)dPp});
+            cudaMemcpyAsync(dA, hA.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(dPp, hPp.data(), sizeof(double *) * nb, cudaMemcpyHostToDevice, st);
+            d.d_AT[slot][col] = dA;
+            d.d_PpT[slot][col] = dPp;
+            DFPArgs x{};
+            x.n = d.n;
+            x.nblk = (int)nb;
+            x.ngrp = (DF_WMAX + DFP_S - 1) / DFP_S;  // unit columns in groups of DFP_S
+            x.P = P;
+            x.bi0 = d.d_bi0[col];
+            x.bW = d.d_bW[col];
+            x.ET = dE;
+            x.PI = dP;
+            x.tau = tau;
+            x.op_me = df_op(d, col);
+            x.op_ot = df_op(d, 1 - col);
+            x.setup = 1;
+            const unsigned grid = (unsigned)(nb * x.ngrp * P);
+            const size_t s2 = sizeof(double) * (2 * DFP_HALF + 2 * DFP_TILE);  // matrix halves + 2 tiles
+            cudaFuncSetAttribute(dfp_fwd_kernel<0, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+            cudaFuncSetAttribute(dfp_bwd_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+            x.setup_out = dA;
+            dfp_fwd_kernel<0, 0, 2><<<grid, DFP_T, s2, st>>>(x);
+            x.setup_out = dPp;
+            dfp_bwd_kernel<0, 2><<<grid, DFP_T, s2, st>>>(x);
+        }
     }
     if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
         err = "full-tensor factorisation failed";
@@ -1616,7 +1665,7 @@ inline void dd_free(DDData &d) {
     }
     if (d.gbuf) cudaFree(d.gbuf);
     if (d.gtot) cudaFree(d.gtot);
-    double *bufs[] = {d.rhon, d.rhof, d.Z, d.dxf, d.dyf, d.gs, d.tup, d.bnd};
+    double *bufs[] = {d.rhon, d.rhof, d.Z, d.dxf, d.dyf, d.gs, d.tup, d.bnd, d.dfp_tl, d.dfp_by, d.dfp_bx, d.dfp_ys};
     for (double *p : bufs)
         if (p) cudaFree(p);
     for (int c = 0; c < 2; ++c) {
@@ -1631,6 +1680,101 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
                    unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err, long long &launches,
                    double src_amp, int src) {
     const int n = d.n;
+    if (d.full && d.dfpart) {
+        const int P = (n + DFP_M - 1) / DFP_M, ngrp = (int)((B + DFP_S - 1) / DFP_S);
+        const int nbmax = (int)std::max(d.bi0[0].size(), d.bi0[1].size());
+        const long long bgs = (long long)nbmax * ngrp;
+        if (bgs > d.dcap) {
+            double *bufs[] = {d.dfp_tl, d.dfp_by, d.dfp_bx, d.dfp_ys};
+            for (double *q : bufs)
+                if (q) cudaFree(q);
+            d.dfp_tl = d.dfp_by = d.dfp_bx = d.dfp_ys = nullptr;
+            d.dcap = 0;
+            const size_t tile = sizeof(double) * DF_WMAX * DFP_S;
+            if (cudaMalloc(&d.dfp_tl, tile * bgs * P) != cudaSuccess ||
+                cudaMalloc(&d.dfp_by, tile * bgs * P) != cudaSuccess ||
+                cudaMalloc(&d.dfp_bx, tile * bgs * P) != cudaSuccess ||
+                cudaMalloc(&d.dfp_ys, tile * bgs * n) != cudaSuccess) {
+                err = "cudaMalloc (full-tensor partition scratch) failed";
+                return PRS_ECUDA;
+            }
+            d.dcap = bgs;
+            ++d.gen;
+        }
+        const size_t s2 = sizeof(double) * (2 * DFP_HALF + 2 * DFP_TILE), s3 = s2;  // matrix halves + 2 tiles
+        for (int stage = 0; stage < 2; ++stage) {
+            DFPArgs x{};
+            x.U = in;
+            x.V = out;
+            x.vol = (long long)n * n;
+            x.n = n;
+            x.B = (int)B;
+            x.stage = stage;
+            x.nblk = (int)d.bi0[stage].size();
+            x.ngrp = ngrp;
+            x.P = P;
+            x.bi0 = d.d_bi0[stage];
+            x.bW = d.d_bW[stage];
+            x.ET = d.d_ET[slot][stage];
+            x.PI = d.d_PI[slot][stage];
+            x.AT = d.d_AT[slot][stage];
+            x.PpT = d.d_PpT[slot][stage];
+            x.tau = d.tau[slot];
+            x.c = d.c;
+            x.op_me = df_op(d, stage);
+            x.op_ot = df_op(d, 1 - stage);
+            x.src_amp = src_amp;
+            x.sinpi = d.sinpi;
+            x.ta = ta;
+            x.epi = epi;
+            x.e_gc = gc;
+            x.e_gcache = gcache;
+            x.e_delta = delta;
+            x.e_traj = traj;
+            x.e_red = red;
+            x.tl = d.dfp_tl;
+            x.bnd_y = d.dfp_by;
+            x.bnd_x = d.dfp_bx;
+            x.ys = d.dfp_ys;
+            void (*f0)(DFPArgs) = nullptr, (*f1)(DFPArgs) = nullptr, (*b0)(DFPArgs) = nullptr, (*b1)(DFPArgs) = nullptr;
+            const int dr = scheme == PRS_DR;
+#define DK(D, S_)                              \
+    if (dr == D && src == S_) {                \
+        f0 = dfp_fwd_kernel<D, S_, 0>;         \
+        f1 = dfp_fwd_kernel<D, S_, 1>;         \
+        b0 = dfp_bwd_kernel<D, 0>;             \
+        b1 = dfp_bwd_kernel<D, 1>;             \
+    }
+            DK(0, 0) DK(0, 1) DK(1, 0) DK(1, 1)
+#undef DK
+            void (*fs[4])(DFPArgs) = {f0, f1, dfp_scan_kernel<1>, dfp_scan_kernel<0>};
+            for (auto fk : fs) cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+            cudaFuncSetAttribute(b0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
+            cudaFuncSetAttribute(b1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
+            const unsigned grid = (unsigned)(x.nblk * ngrp * P), sgrid = (unsigned)(x.nblk * ngrp);
+            if (prof && prs_internal_prof_begin(prof) != PRS_OK) return PRS_ECUDA;
+            f0<<<grid, DFP_T, s2, st>>>(x);
+            dfp_scan_kernel<1><<<sgrid, DFP_T, s2, st>>>(x);
+            f1<<<grid, DFP_T, s2, st>>>(x);
+            b0<<<grid, DFP_T, s3, st>>>(x);
+            dfp_scan_kernel<0><<<sgrid, DFP_T, s2, st>>>(x);
+            b1<<<grid, DFP_T, s3, st>>>(x);
+            launches += 6;
+            const cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                err = std::string("full-tensor partitioned stage: ") + cudaGetErrorString(e);
+                return PRS_ECUDA;
+            }
+            if (prof) {
+                // algorithmic fp64 flops: the sequential block Thomas (two dense W x W mat-vecs per
+                // block row and state); the partitioned form does twice this plus the scans
+                double flops = 0.0;
+                for (int w : d.bW[stage]) flops += (double)n * (4.0 * w * w + 20.0 * w);
+                if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
+            }
+        }
+        return PRS_OK;
+    }
     if (d.full) {
         for (int stage = 0; stage < 2; ++stage) {
             DFStageArgs a{};

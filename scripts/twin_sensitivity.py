@@ -1,11 +1,14 @@
 #!/usr/bin/env python
-"""Rounding sensitivity of a reduced-parity twin's parareal iteration, from the CPU oracle alone
-(R27).  Two fp64 implementations that are each correct differ by rounding at every
-step; the iteration carries such differences forward with its own amplification.  This script
-measures that amplification directly: it runs the oracle on U_0 and on U_0 perturbed by one
-relative unit of rounding (U_0 (1 + eps64 z), z = +-1 seeded), digests both runs exactly as
-scripts/gen_twin_digests.py does, and writes per k the largest digest difference normalised
-as in the twin test.  Calls only ``oracle`` and ``synth``.
+"""Rounding floor of a reduced-parity twin's parareal iteration, from the CPU oracle alone
+(R27).  Two fp64 implementations of the same literal algorithm that are each correct
+differ by rounding in every step; the iteration carries those differences forward with its own
+amplification.  This script measures that floor with the oracle itself: it compiles oracle.c a
+second time with FMA contraction (gcc -O2 -mfma -ffp-contract=fast: every a*b+c of the literal
+algorithm rounded once instead of twice -- the same algorithm, another correct rounding), runs
+that build on the twin's problem for k = 0..kmax, digests the iterates exactly as
+scripts/gen_twin_digests.py did for the stored digests (tests/golden/twins/<name>.npz, the
+uncontracted build) and writes per k the largest digest difference, normalised as in the twin
+test, to tests/golden/twins/<name>_floor.json.  Calls only ``oracle`` (rebuilt) and ``synth``.
 
     python scripts/twin_sensitivity.py c4r_DR-DR [kmax]
 """
@@ -14,6 +17,7 @@ from __future__ import annotations
 import json
 import math
 import os
+import subprocess
 import sys
 import time
 
@@ -28,38 +32,45 @@ import synth  # noqa: E402
 from gen_twin_digests import twins  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "twins")
+FLAGS = ["-O2", "-mfma", "-ffp-contract=fast", "-fno-fast-math", "-std=c11"]
 
 
-def run(o, p, u0, kmax, idx, signs):
-    traj = o.coarse_sweep(u0)
-    digs = [synth.digest(traj, idx, signs)]
-    for _ in range(kmax):
-        traj = o.iteration(traj)
-        digs.append(synth.digest(traj, idx, signs))
-    return digs
+def contracted_oracle():
+    so = os.path.join("/tmp", f"liboracle_fma_{os.getpid()}.so")
+    subprocess.check_call(["gcc"] + FLAGS + ["-shared", "-fPIC", "-pthread", "-o", so] + oracle._SRC + ["-lm"])
+    oracle._SO = so
+    oracle.build = lambda force=False: so
+    oracle._lib = None
+    return so
 
 
 def main(name, kmax):
     p, _, _ = twins()[name]
+    ref = np.load(os.path.join(OUT, f"{name}.npz"))
+    kmax = min(kmax, len(ref["upd"]))
+    contracted_oracle()
     o = oracle.Oracle(p)
     oracle.set_threads(int(os.environ.get("ORACLE_THREADS", oracle.host_threads())))
-    idx, signs = synth.sample_indices(p.npts), synth.projection_signs(p.npts)
+    idx, signs = ref["idx"], synth.projection_signs(p.npts)
     u0 = synth.initial_state(p)
-    z = np.where(np.random.default_rng(12345).random(u0.shape) < 0.5, -1.0, 1.0)
-    u1 = u0 * (1.0 + 2.0 ** -52 * z)
     t0 = time.time()
-    a, b = run(o, p, u0, kmax, idx, signs), run(o, p, u1, kmax, idx, signs)
+    traj = o.coarse_sweep(u0)
     scale0 = float(np.max(np.abs(u0)))
-    sens = []
+    floor = []
     for k in range(kmax + 1):
-        scale = max(scale0, float(np.max(a[k]["inf"])))
-        es = float(np.max(np.abs(a[k]["samples"] - b[k]["samples"]))) / scale
-        ep = float(np.max(np.abs(a[k]["proj"] - b[k]["proj"]))) / (scale * math.sqrt(p.npts))
-        sens.append(max(es, ep))
-        print(f"{name}: k = {k} relative digest change {sens[-1]:.3e}", flush=True)
-    meta = {"name": name, "kmax": kmax, "perturbation": "U_0 (1 + 2^-52 z), z = +-1 (rng 12345)",
-            "sensitivity": sens, "seconds": time.time() - t0, "script": "scripts/twin_sensitivity.py"}
-    with open(os.path.join(OUT, f"{name}_sens.json"), "w") as f:
+        if k > 0:
+            traj = o.iteration(traj)
+        g = synth.digest(traj, idx, signs)
+        scale = max(scale0, float(np.max(ref["inf"][k])))
+        es = float(np.max(np.abs(g["samples"] - ref["samples"][k]))) / scale
+        ep = float(np.max(np.abs(g["proj"] - ref["proj"][k]))) / (scale * math.sqrt(p.npts))
+        floor.append(max(es, ep))
+        print(f"{name}: k = {k} contracted vs stored oracle digests {floor[-1]:.3e} ({time.time() - t0:.0f} s)",
+              flush=True)
+    meta = {"name": name, "kmax": kmax, "flags": " ".join(FLAGS), "floor": floor,
+            "seconds": time.time() - t0, "script": "scripts/twin_sensitivity.py",
+            "what": "max normalised digest difference between the oracle built with and without FMA contraction"}
+    with open(os.path.join(OUT, f"{name}_floor.json"), "w") as f:
         json.dump(meta, f, indent=1)
 
 
