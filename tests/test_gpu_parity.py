@@ -939,6 +939,38 @@ def test_full_tensor_parareal_matches_oracle_every_iteration(p):
     _parareal_vs_oracle(p)
 
 
+@pytest.mark.parametrize("impl", ["partitioned", "sequential"])
+def test_full_tensor_batched_steps_two_state_groups(impl, monkeypatch):
+    """The partitioned block Thomas (dfpart.cuh) in the fine sweep's launch configuration over
+    B = 21 states -- two groups of 16, the second partial -- on 3 row partitions (n = 160, the
+    last one short), fine FIE / DR and coarse steps, each state against the oracle; and the
+    sequential df_stage_kernel (PRS_DFPART=0) on the same cases."""
+    if impl == "sequential":
+        monkeypatch.setenv("PRS_DFPART", "0")
+    p = Problem(dim=2, n=160, c=1.0, coef=2, split=1, dd_strips=4, dd_overlap=8, dd_ramp=1, source=1, N=22, s=3,
+                G=FIE, F=DR)
+    prs = prs_mod()
+    ctx = prs.Context(p)
+    o = oracle.Oracle(p)
+    B = 21
+    us = np.stack([(1.0 + 0.1 * b) * rand_field(p, 700 + b) for b in range(B)])
+    du = dev(us)
+    out = torch.empty_like(du)
+    dt, dT = p.T / (p.N * p.s), p.T / p.N
+    for which, j in ((1, 2), (0, 0)):
+        ctx.step_batch(which, 1, j, du, out, B)
+        got = host(out)
+        for b in range(B):
+            if which == 1:
+                tau, sch, tn = dt, p.F, float((1 + b) * p.s + j + 1) * dt
+            else:
+                tau, sch, tn = dT, p.G, float(1 + b + 1) * dT
+            want = o.step(sch, tau, tn, us[b])
+            scales = (want, us[b], tau * o.apply(-1, us[b])) if sch == DR else (want, us[b])
+            assert nerr(got[b], want, *scales) <= TOL, (which, b)
+    ctx.close()
+
+
 def test_full_tensor_full_size_steps():
     """The full tensor on c4's DD geometry at full size (1024^2, 8 strips, 8-cell overlap): one
     coarse and one fine step of each scheme against the oracle."""
