@@ -1397,6 +1397,9 @@ struct DDData {
     long long gcap = 0;
     // split stage (default; PRS_DDSPLIT=0: the single-kernel stage with the L2 exchange)
     bool split = true;
+    bool two = true;            // split stage: the batch's two halves on two streams (PRS_DD2S=0: one)
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
     double *gs = nullptr, *tup = nullptr, *bnd = nullptr;
     long long scap = 0;         // block-states (B x blocks) the split scratch holds
     // full diffusion tensor (coef_kind 2, ddfull.cuh): d tables and per (slot, colour) the
@@ -1498,6 +1501,8 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     d.gx = !(clv && clv[0] == '1');
     const char *spv = getenv("PRS_DDSPLIT");
     d.split = d.gx && !(spv && spv[0] == '0');
+    const char *d2v = getenv("PRS_DD2S");
+    d.two = !(d2v && d2v[0] == '0');
     const char *dpv = getenv("PRS_DFPART");
     d.dfpart = !(dpv && dpv[0] == '0');
     int dev = 0;
@@ -1659,6 +1664,9 @@ inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
 }
 
 inline void dd_free(DDData &d) {
+    if (d.st2) cudaStreamDestroy(d.st2);
+    for (auto e : d.ev)
+        if (e) cudaEventDestroy(e);
     for (auto &v : d.store) {
         for (double *p : v) cudaFree(p);
         v.clear();
@@ -1675,11 +1683,66 @@ inline void dd_free(DDData &d) {
 }
 
 // one DD step (two colour stages) on B states: in -> out
+inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, double *out, long long B,
+                        const TimeArgs &ta, int epi, const double *gc, double *gcache, const double *delta,
+                        double *traj, unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err,
+                        long long &launches, double src_amp, int src, long long soff = 0, long long Btot = -1);
+
+// one DD step (two colour stages) on B states: in -> out.  Split DD stage with a batch of at least
+// two DD_HALFB groups: the two halves of the batch run on two streams (fork / join), so that the
+// passes of one half (e.g. its GEMMs) meet the other half's loads and walks on the SMs instead
+// of every CTA of a launch moving through the same phase at the same time
+constexpr int DD_HALFB = 8;
 inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *out, long long B, const TimeArgs &ta,
                    int epi, const double *gc, double *gcache, const double *delta, double *traj,
                    unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err, long long &launches,
                    double src_amp, int src) {
+    if (!(d.two && d.split && !d.full && B >= 2 * DD_HALFB))
+        return dd_step_impl(d, scheme, slot, in, out, B, ta, epi, gc, gcache, delta, traj, red, st, prof, err,
+                            launches, src_amp, src);
+    if (!d.st2) {
+        if (cudaStreamCreateWithFlags(&d.st2, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&d.ev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&d.ev[1], cudaEventDisableTiming) != cudaSuccess) {
+            err = "DD second stream";
+            return PRS_ECUDA;
+        }
+    }
+    const long long B1 = B / 2, B2 = B - B1;
+    if (prof && prs_internal_prof_begin(prof) != PRS_OK) return PRS_ECUDA;
+    if (cudaEventRecord(d.ev[0], st) != cudaSuccess || cudaStreamWaitEvent(d.st2, d.ev[0], 0) != cudaSuccess) {
+        err = "DD fork";
+        return PRS_ECUDA;
+    }
+    TimeArgs ta2 = ta;
+    ta2.slice0 = ta.slice0 + B1 * ta.sstride;
+    const long long vol = (long long)d.n * d.n;
+    int rc = dd_step_impl(d, scheme, slot, in, out, B1, ta, epi, gc, gcache, delta, traj, red, st, nullptr, err,
+                          launches, src_amp, src, 0, B);
+    if (rc != PRS_OK) return rc;
+    rc = dd_step_impl(d, scheme, slot, in + B1 * vol, out + B1 * vol, B2, ta2, epi, gc ? gc + B1 * vol : nullptr,
+                      gcache, delta, traj, red, d.st2, nullptr, err, launches, src_amp, src, B1, B);
+    if (rc != PRS_OK) return rc;
+    if (cudaEventRecord(d.ev[1], d.st2) != cudaSuccess || cudaStreamWaitEvent(st, d.ev[1], 0) != cudaSuccess) {
+        err = "DD join";
+        return PRS_ECUDA;
+    }
+    if (prof) {
+        double flops = 0.0;
+        for (int stage = 0; stage < 2; ++stage)
+            for (int w : d.bW[stage]) flops += (double)w * d.n * (4.0 * w + 10.0);
+        // both colour stages of the step in one interval: accounted as two stage launches
+        if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
+    }
+    return PRS_OK;
+}
+
+inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, double *out, long long B,
+                        const TimeArgs &ta, int epi, const double *gc, double *gcache, const double *delta,
+                        double *traj, unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err,
+                        long long &launches, double src_amp, int src, long long soff, long long Btot) {
     const int n = d.n;
+    if (Btot < 0) Btot = B;
     if (d.full && d.dfpart) {
         const int P = (n + DFP_M - 1) / DFP_M, ngrp = (int)((B + DFP_S - 1) / DFP_S);
         const int nbmax = (int)std::max(d.bi0[0].size(), d.bi0[1].size());
@@ -1862,24 +1925,27 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
         a.e_red = red;
         const long long ntasks = B * a.nblk * CL;
         if (d.split) {
-            if (B * a.nblk > d.scap) {
+            const long long ntot = Btot * a.nblk * CL;  // the whole batch's tasks (two-stream halves share)
+            if (Btot * a.nblk > d.scap) {
                 double *bufs[] = {d.gs, d.tup, d.bnd};
                 for (double *p : bufs)
                     if (p) cudaFree(p);
                 d.gs = d.tup = d.bnd = nullptr;
                 d.scap = 0;
-                if (cudaMalloc(&d.gs, sizeof(double) * DD_WMAX * (size_t)n * B * a.nblk) != cudaSuccess ||
-                    cudaMalloc(&d.tup, sizeof(double) * 5 * DD_WMAX * 2 * ntasks) != cudaSuccess ||
-                    cudaMalloc(&d.bnd, sizeof(double) * 2 * DD_WMAX * 2 * ntasks) != cudaSuccess) {
+                if (cudaMalloc(&d.gs, sizeof(double) * DD_WMAX * (size_t)n * Btot * a.nblk) != cudaSuccess ||
+                    cudaMalloc(&d.tup, sizeof(double) * 5 * DD_WMAX * 2 * ntot) != cudaSuccess ||
+                    cudaMalloc(&d.bnd, sizeof(double) * 2 * DD_WMAX * 2 * ntot) != cudaSuccess) {
                     err = "cudaMalloc (DD split scratch) failed";
                     return PRS_ECUDA;
                 }
-                d.scap = B * a.nblk;
+                d.scap = Btot * a.nblk;
                 ++d.gen;
             }
-            a.gs = d.gs;
-            a.tup = d.tup;
-            a.bnd = d.bnd;
+            // (a second half of the batch takes the scratch after the first half's)
+            const long long toff = soff * a.nblk * CL;
+            a.gs = d.gs + (size_t)DD_WMAX * n * soff * a.nblk;
+            a.tup = d.tup + (size_t)5 * DD_WMAX * 2 * toff;
+            a.bnd = d.bnd + (size_t)2 * DD_WMAX * 2 * toff;
             a.ntasks = (int)ntasks;
             void (*k1)(DDStageArgs) = nullptr, (*k2)(DDStageArgs) = nullptr;
             const int dr = scheme == PRS_DR;
