@@ -46,10 +46,11 @@ def lib() -> ctypes.CDLL:
     """Load libprs.so (fails loudly if it has not been built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(SO):
+        so = os.environ.get("PRS_SO", SO)  # (test hook: the checked build libprs_chk.so)
+        if not os.path.exists(so):
             raise ImportError(f"{SO} is missing: run paper_2502_08370_b200._build.build() "
                               "(or __graft_entry__.build()); there is no fallback path")
-        L = ctypes.CDLL(SO)
+        L = ctypes.CDLL(so)
         V, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
         PI, PD, PL = ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), \
             ctypes.POINTER(ctypes.c_longlong)

@@ -22,16 +22,20 @@ def deps():
         [os.path.join(ROOT, "include", "prs.h"), __file__]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+SO_CHK = os.path.join(HERE, "libprs_chk.so")  # -DPRS_CHECKS: bounds / protocol checks (test builds)
+
+
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    so = SO_CHK if checks else SO
     newest = max(os.path.getmtime(f) for f in deps())
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
-        return SO
-    cmd = [NVCC] + FLAGS + ["-o", SO + ".tmp"] + sources() + ["-ldl"]
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= newest:
+        return so
+    cmd = [NVCC] + FLAGS + (["-DPRS_CHECKS"] if checks else []) + ["-o", so + ".tmp"] + sources() + ["-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":

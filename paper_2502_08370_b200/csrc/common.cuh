@@ -20,9 +20,30 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace prs {
 namespace cg = cooperative_groups;
+
+// Checked build (-DPRS_CHECKS, libprs_chk.so; compute-sanitizer is not available on the GPU
+// pool): bounds of every shared-memory async-copy destination and scratch index of the async
+// paths, and bounded waits on every mbarrier -- a violated check or a wait that outlives any
+// legitimate one prints where and traps (the launch fails with an error instead of corrupting
+// memory or hanging the device).  Production builds compile the checks away.
+#ifdef PRS_CHECKS
+#define PRS_CHECK(cond, what)                                                                       \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("PRS_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,   \
+                   (int)blockIdx.x, (int)threadIdx.x);                                              \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define PRS_CHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
 
 constexpr int LCH = 16;  // elements per chunk (per thread per line)
 constexpr int LCP = LCH + 1;  // padded chunk stride
@@ -180,6 +201,22 @@ __device__ __forceinline__ void mbar_arrive_expect(unsigned long long *mb, unsig
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long *mb, unsigned parity) {
     const unsigned a = smem_u32(mb);
+#ifdef PRS_CHECKS
+    for (long long it = 0;; ++it) {
+        unsigned ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        PRS_CHECK(it < (1ll << 22), "mbarrier wait outlived any legitimate one");
+    }
+#else
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -189,6 +226,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *mb, unsigned parit
         "}\n" ::"r"(a),
         "r"(parity)
         : "memory");
+#endif
 }
 // st.async of a double2 into CTA `rank`'s copy of the local shared object `dst`, completing
 // tx bytes on that CTA's mbarrier `mb` (local address of the same object)

@@ -258,6 +258,7 @@ struct DDStageArgs {
     // split stage (dd_p1 / dd_scan / dd_p2): per task the transformed tile G [R][DD_WMAX], the
     // piece's transfer tuple [5][DD_WMAX] and its boundary values y_in, x_in [2][DD_WMAX]
     double *gs, *tup, *bnd;
+    long long gs_end, tup_end, bnd_end;  // PRS_CHECKS: element counts of gs / tup / bnd from their pointers
     int abl;  // diagnostic build (-DPRS_DD_TIMING) only: PRS_DD_ABL bit 0 skips the GEMMs, bit 1 the walks
 };
 
@@ -1142,6 +1143,7 @@ __device__ __forceinline__ void dd_piece_walks(const DDStageArgs &a, double *T, 
                     idp = id[i];
                 }
         }
+        PRS_CHECK((tk + 1) * 5 * DD_WMAX <= a.tup_end, "DD tuple outside the scratch");
         double *tp = a.tup + tk * 5 * DD_WMAX + am;
         tp[0] = al;
         tp[DD_WMAX] = be;
@@ -1224,6 +1226,7 @@ template <class SY>
 __device__ __forceinline__ void dd_p1_post(const DDStageArgs &a, double *T, const DDTask &t, int tid, SY sync,
                                            const DDWalkPre &wp) {
     double *G = a.gs + (t.task * a.n + t.r0) * (long long)DD_WMAX;
+    PRS_CHECK((t.task * a.n + t.r0 + t.nrow) * (long long)DD_WMAX <= a.gs_end, "DD G tile outside the scratch");
     const bool bulk = (t.W & 1) == 0;  // rows of W doubles are 16-byte multiples
     if (bulk) {
         if (tid == 0) {
@@ -1255,6 +1258,8 @@ __device__ __forceinline__ void dd_p2_pre(const DDStageArgs &a, double *T, const
                                           unsigned long long *mbg, unsigned par) {
     const DDWalkPre wp = dd_walk_prefetch<0>(a, t.blk, t.tk, tid);  // in flight with the G copies
     const double *G = a.gs + (t.task * a.n + t.r0) * (long long)DD_WMAX;
+    PRS_CHECK((t.task * a.n + t.r0 + t.nrow) * (long long)DD_WMAX <= a.gs_end, "DD G tile outside the scratch");
+    PRS_CHECK(t.nrow <= DD_RMAX && t.W <= DD_WMAX, "DD tile shape");
     const bool bulk = (t.W & 1) == 0;
     const int lane = tid & 31;
     if (bulk && tid == 0) {
@@ -1946,6 +1951,9 @@ inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, doubl
             a.gs = d.gs + (size_t)DD_WMAX * n * soff * a.nblk;
             a.tup = d.tup + (size_t)5 * DD_WMAX * 2 * toff;
             a.bnd = d.bnd + (size_t)2 * DD_WMAX * 2 * toff;
+            a.gs_end = (long long)DD_WMAX * n * (d.scap - soff * a.nblk);
+            a.tup_end = (long long)5 * DD_WMAX * 2 * (d.scap * CL - toff);
+            a.bnd_end = (long long)2 * DD_WMAX * 2 * (d.scap * CL - toff);
             a.ntasks = (int)ntasks;
             void (*k1)(DDStageArgs) = nullptr, (*k2)(DDStageArgs) = nullptr;
             const int dr = scheme == PRS_DR;

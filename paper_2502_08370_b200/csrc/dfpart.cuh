@@ -159,6 +159,7 @@ __device__ __forceinline__ void dfp_issue_half(DFPStream &st, const double *MT, 
     }
     const int off = dfp_half_off(MT, W, h);
     const unsigned bytes = (unsigned)((((size_t)(k1 - k0) * W + off) * sizeof(double) + 15) & ~(size_t)15);
+    PRS_CHECK(bytes <= DFP_HALF * sizeof(double), "full-tensor matrix half larger than its shared buffer");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     mbar_arrive_expect(st.mb + h, bytes);
     const char *src = reinterpret_cast<const char *>(MT + (long long)k0 * W - off);
@@ -269,6 +270,7 @@ struct DFPTask {
         i0 = x.bi0[blk];
         a = p * DFP_M;
         m = min(DFP_M, x.n - a);
+        PRS_CHECK(blk < x.nblk && W <= DF_WMAX && m > 0 && i0 >= 0 && i0 + W <= x.n, "full-tensor task");
     }
 };
 

@@ -142,6 +142,9 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(const __grid_constant__ 
     // TMA: tensor row (128-byte row = chunk) of this CTA's half of batch row g / pivot row j
     auto trow_state = [&](long long g) { return (g >> 12) * (a.vol / LCH) + (g & 4095) * (X7N / LCH) + crank * X7T; };
     auto tma_load = [&](const CUtensorMap *tm, long long tr, double *dst, unsigned long long *mb) {
+        PRS_CHECK(dst >= smem && dst + X7S <= smem + 6 * X7S && ((reinterpret_cast<uintptr_t>(dst) & 1023) == 0),
+                  "xpass7 TMA destination outside the 1024-aligned slots");
+        PRS_CHECK(tr >= 0 && tr + X7T <= a.nrows * (X7N / LCH), "xpass7 TMA row");
         mbar_arrive_expect(mb, (unsigned)(X7S * sizeof(double)));
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
