@@ -115,6 +115,70 @@ struct DDBlock {
     double *Q = nullptr, *QT = nullptr, *theta = nullptr, *idy = nullptr;  // per tau slot
 };
 
+// double-double arithmetic (setup only): a value hi + lo with |lo| <= ulp(hi) / 2
+struct DDd {
+    double hi, lo;
+};
+__device__ __forceinline__ DDd ddd_two_sum(double a, double b) {
+    const double s = a + b, bb = s - a;
+    return DDd{s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ DDd ddd_norm(double hi, double lo) {
+    const double s = hi + lo;
+    return DDd{s, lo - (s - hi)};
+}
+__device__ __forceinline__ DDd ddd_add(DDd a, DDd b) {
+    const DDd s = ddd_two_sum(a.hi, b.hi);
+    return ddd_norm(s.hi, s.lo + a.lo + b.lo);
+}
+__device__ __forceinline__ DDd ddd_mul_d(DDd a, double b) {
+    const double p = a.hi * b;
+    return ddd_norm(p, fma(a.hi, b, -p) + a.lo * b);
+}
+__device__ __forceinline__ DDd ddd_div(DDd a, DDd b) {
+    const double q1 = a.hi / b.hi;
+    const DDd r = ddd_add(a, ddd_mul_d(b, -q1));
+    const double q2 = r.hi / b.hi;
+    const DDd q = ddd_norm(q1, q2);
+    const DDd r2 = ddd_add(r, ddd_mul_d(b, -q2));
+    return ddd_norm(q.hi, q.lo + r2.hi / b.hi);
+}
+// s += a b (a, b doubles)
+__device__ __forceinline__ void dd_acc(DDd &s, double a, double b) {
+    const double p = a * b, pe = fma(a, b, -p);
+    const DDd t = ddd_two_sum(s.hi, p);
+    s = ddd_norm(t.hi, t.lo + s.lo + pe);
+}
+
+// theta_a and the pivots of mode a's y system theta_a I - tau Y (diagonal theta_a + 2 s, off -s,
+// s = tau / h^2): id_l = 1 / d_l, and in theta[W + a] the row from which they are constant.
+// The recurrence d_l = theta_a + 2 s - s^2 / d_{l-1} runs in double-double and only id_l is
+// rounded: in fp64, theta_a + 2 s alone rounds by eps s -- at c4's coarse step (s = 3.3e4) a
+// COHERENT shift of every low mode's theta_a (~16) by ~1e-12 of itself, which the smooth part of
+// the solution takes over whole (GPU 4e-12 off the extended-precision step, the oracle, whose
+// band-matrix entries are exact here, 2e-13).  Rounding id_l alone perturbs the implied
+// matrix by independent +-eps dipoles per row, which smooth solutions do not feel.
+__device__ inline void dd_mode_pivots(int n, int W, int a, DDd th, double s, double *theta, double *idy) {
+    theta[a] = th.hi;
+    const DDd bd = ddd_add(th, DDd{2.0 * s, 0.0});
+    const DDd s2 = ddd_norm(s * s, fma(s, s, -s * s));
+    DDd d = bd;
+    double prev = 0.0;
+    int lc = 0;  // last row whose pivot differs from the row before: rows >= lc share one value
+    for (int l = 0; l < n; ++l) {
+        if (l > 0) {
+            const DDd q = ddd_div(s2, d);
+            d = ddd_add(bd, DDd{-q.hi, -q.lo});
+        }
+        const DDd idd = ddd_div(DDd{1.0, 0.0}, d);
+        const double id = idd.hi + idd.lo;
+        if (l > 0 && id != prev) lc = l;
+        prev = id;
+        idy[(long long)l * W + a] = id;
+    }
+    theta[W + a] = (double)lc;  // (the recurrence reaches its fixed point in a few hundred rows)
+}
+
 __global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, int W, const double *rhon,
                                                                const double *rhof, double tau, double h2inv,
                                                                double c, double *Z, double *Q, double *QT,
@@ -202,28 +266,101 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, i
         }
     }
     // eigenvalues on the diagonal; Q = R^{-1/2} Z; pivots of theta_a + 2 s, off -s (s = tau/h^2)
-    const double s = tau * h2inv;
-    for (int a = tid; a < W; a += blockDim.x) {
-        const double th = C[a * W + a];
-        theta[a] = th;
-        const double bd = th + 2.0 * s;
-        double d = bd, prev = 0.0;
-        int lc = 0;  // last row whose pivot differs from the row before: rows >= lc share one value
-        for (int l = 0; l < n; ++l) {
-            if (l > 0) d = bd - s * s / d;
-            const double id = 1.0 / d;
-            if (l > 0 && id != prev) lc = l;
-            prev = id;
-            idy[(long long)l * W + a] = id;
-        }
-        theta[W + a] = (double)lc;  // (the recurrence reaches its fixed point in a few hundred rows)
-    }
+    for (int a = tid; a < W; a += blockDim.x) dd_mode_pivots(n, W, a, DDd{C[a * W + a], 0.0}, tau * h2inv, theta, idy);
     for (int e = tid; e < W * W; e += blockDim.x) {
         const int r = e / W, k = e % W;
         const double q = Z[e] / sqrt(rhon[i0 + r]);
         Q[e] = q;             // Q[i][a]
         QT[k * W + r] = q;    // QT[a][i]
     }
+}
+
+// ------------------------------------------------ refinement of the eigenbasis ---
+// Jacobi in fp64 leaves each eigenvector of C off by ~eps ||C|| / gap: at c4's coarse step
+// (tau / h^2 = 3.3e4, ||C|| ~ 2e6, low-mode gaps ~ 50) that is ~1e-11, and the block solve
+// inherits it (one coarse step 7e-12 of |U| off the extended-precision value, against the
+// oracle's band elimination at 2e-13).  One Newton step on the generalised problem (the
+// Ogita-Aishima refinement with R in place of I) restores full accuracy: with X = Q from Jacobi,
+//     Ms = X^T S X,  Mr = X^T R X   (products exact to double-double: the off-diagonal terms
+//                                     sought are ~eps ||C|| residues of sums of size ||C||),
+//     theta_a = Ms_aa / Mr_aa,  E_aa = (1 - Mr_aa) / 2,
+//     E_ab = (Ms_ab - theta_b Mr_ab) / (theta_b - theta_a)   (a != b; E_ab = -Mr_ab / 2 for a
+//            relative gap below 1e-6, where the coupling left behind is below eps theta),
+//     Q' = X (I + E),
+// after which Q'^T R Q' = I and Q'^T S Q' = Theta up to (eps ||C|| / gap)^2 and the rounding
+// of Q' itself.  One CTA per block, once per tau (setup).
+__global__ void __launch_bounds__(DD_FTHREADS) dd_refine_kernel(int n, int i0, int W, const double *rhon,
+                                                               const double *rhof, double tau, double h2inv,
+                                                               double c, double *scr, double *Q, double *QT,
+                                                               double *theta, double *idy) {
+    const int tid = threadIdx.x;
+    const int WW = W * W;
+    double *Thi = scr, *Tlo = scr + WW, *Ms = scr + 2 * WW, *Mr = scr + 3 * WW;
+    __shared__ double th[DD_WMAX], thl[DD_WMAX], dr[DD_WMAX];
+    const double s = tau * h2inv;
+    // T = S X (S tridiagonal, the block rows of I - tau A_j, dd.cuh header) in double-double
+    for (int e = tid; e < WW; e += blockDim.x) {
+        const int i = e / W, gi = i0 + i;
+        DDd t{0.0, 0.0};
+        dd_acc(t, 1.0 + s * (rhof[gi] + rhof[gi + 1]) + tau * c * rhon[gi], Q[e]);
+        if (i > 0) dd_acc(t, -s * rhof[gi], Q[e - W]);
+        if (i + 1 < W) dd_acc(t, -s * rhof[gi + 1], Q[e + W]);
+        Thi[e] = t.hi;
+        Tlo[e] = t.lo;
+    }
+    __syncthreads();
+    // Ms = X^T T, Mr = X^T R X (a <= b), double-double
+    for (int e = tid; e < WW; e += blockDim.x) {
+        const int a = e / W, b = e % W;
+        if (b < a) continue;
+        DDd ms{0.0, 0.0}, mr{0.0, 0.0};
+        for (int i = 0; i < W; ++i) {
+            const double xa = Q[i * W + a], xb = Q[i * W + b];
+            dd_acc(ms, xa, Thi[i * W + b]);
+            ms.lo = fma(xa, Tlo[i * W + b], ms.lo);
+            const double r = rhon[i0 + i];
+            const double pr = xa * r, pre = fma(xa, r, -pr);  // xa rho exactly = pr + pre
+            dd_acc(mr, pr, xb);
+            mr.lo = fma(pre, xb, mr.lo);
+        }
+        if (a == b) {
+            const DDd q = ddd_div(ms, mr);  // the Rayleigh quotient, double-double
+            th[a] = q.hi;
+            thl[a] = q.lo;
+            dr[a] = 0.5 * ((1.0 - mr.hi) - mr.lo);
+        } else {
+            Ms[a * W + b] = Ms[b * W + a] = ms.hi + ms.lo;
+            Mr[a * W + b] = Mr[b * W + a] = mr.hi + mr.lo;
+        }
+    }
+    __syncthreads();
+    // E (into Ms): E_ab = (Ms_ab - theta_b Mr_ab) / (theta_b - theta_a)
+    for (int e = tid; e < WW; e += blockDim.x) {
+        const int a = e / W, b = e % W;
+        double v;
+        if (a == b) {
+            v = dr[a];
+        } else {
+            const double gap = th[b] - th[a];
+            v = (fabs(gap) > 1e-6 * fmax(fabs(th[a]), fabs(th[b]))) ? (Ms[e] - th[b] * Mr[e]) / gap : -0.5 * Mr[e];
+        }
+        Thi[e] = v;  // (T is dead)
+    }
+    __syncthreads();
+    // Q' = X + X E (the correction is ~1e-11 of X: fp64 suffices), into Tlo, then Q, QT
+    for (int e = tid; e < WW; e += blockDim.x) {
+        const int i = e / W, k = e % W;
+        double corr = 0.0;
+        for (int a = 0; a < W; ++a) corr = fma(Q[i * W + a], Thi[a * W + k], corr);
+        Tlo[e] = Q[e] + corr;
+    }
+    __syncthreads();
+    for (int e = tid; e < WW; e += blockDim.x) {
+        const int r = e / W, k = e % W;
+        Q[e] = Tlo[e];
+        QT[k * W + r] = Tlo[e];
+    }
+    for (int a = tid; a < W; a += blockDim.x) dd_mode_pivots(n, W, a, DDd{th[a], thl[a]}, s, theta, idy);
 }
 
 // ------------------------------------------------------------------ stage kernel ---
@@ -1386,7 +1523,8 @@ struct DDData {
     const double *sinpi = nullptr;
     int n = 0, S = 0, ov = 0, ramp = 0, dim = 2;
     double c = 0, h2inv = 0;
-    double *rhon = nullptr, *rhof = nullptr, *Z = nullptr;
+    double *rhon = nullptr, *rhof = nullptr, *Z = nullptr;  // Z: Jacobi eigenvectors + refinement scratch
+    bool refine = true;  // Newton refinement of the eigenbasis (PRS_DDREFINE=0: Jacobi only)
     std::vector<int> bi0[2], bW[2];
     int *d_bi0[2] = {nullptr, nullptr}, *d_bW[2] = {nullptr, nullptr};
     // per tau slot (3) and colour (2): device arrays of per-block pointers + the storage
@@ -1478,7 +1616,7 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     }
     if (cudaMalloc(&d.rhon, sizeof(double) * 2 * d.n) != cudaSuccess ||
         cudaMalloc(&d.rhof, sizeof(double) * 2 * (d.n + 1)) != cudaSuccess ||
-        cudaMalloc(&d.Z, sizeof(double) * DD_WMAX * DD_WMAX) != cudaSuccess) {
+        cudaMalloc(&d.Z, sizeof(double) * 5 * DD_WMAX * DD_WMAX) != cudaSuccess) {
         err = "cudaMalloc (DD tables) failed";
         return PRS_ECUDA;
     }
@@ -1510,6 +1648,8 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     d.two = !(d2v && d2v[0] == '0');
     const char *dpv = getenv("PRS_DFPART");
     d.dfpart = !(dpv && dpv[0] == '0');
+    const char *rfv = getenv("PRS_DDREFINE");
+    d.refine = !(rfv && rfv[0] == '0');
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1638,6 +1778,10 @@ inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
             dd_factor_kernel<<<1, DD_FTHREADS, fsm, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
                                                          d.rhof + col * (d.n + 1), tau, d.h2inv, d.c, d.Z, Q, QT,
                                                          th, idy, 14);
+            if (d.refine)
+                dd_refine_kernel<<<1, DD_FTHREADS, 0, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
+                                                            d.rhof + col * (d.n + 1), tau, d.h2inv, d.c,
+                                                            d.Z + DD_WMAX * DD_WMAX, Q, QT, th, idy);
             hQ[k] = Q;
             hQT[k] = QT;
             hI[k] = idy;
