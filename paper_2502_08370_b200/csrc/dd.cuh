@@ -179,11 +179,38 @@ __device__ inline void dd_mode_pivots(int n, int W, int a, DDd th, double s, dou
     theta[W + a] = (double)lc;  // (the recurrence reaches its fixed point in a few hundred rows)
 }
 
-__global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, int W, const double *rhon,
-                                                               const double *rhof, double tau, double h2inv,
-                                                               double c, double *Z, double *Q, double *QT,
-                                                               double *theta, double *idy, int sweeps) {
+// The m x m generalised problem S x = theta R x of one factorisation (a whole block, m = W, or
+// one half of a folded block, m = W / 2): S tridiagonal (diagonal sd, off-diagonal se), R =
+// diag(sr), assembled by dd_assemble_kernel.
+//   fold 0: the block rows of I - tau A_j:  S_ii = 1 + tau h^-2 (rho(i-1/2) + rho(i+1/2)) +
+//           tau c rho(i),  S_i,i+1 = -tau h^-2 rho(i+1/2),  R = rho(i);
+//   fold 1 / 2 (symmetric / antisymmetric vectors q = [u; +-J u] of a mirror-symmetric block):
+//           the upper W/2 rows of S with the coupling across the centre folded onto the last
+//           diagonal entry (+ / -), everything times 2, so that u^T (2 R) u = q^T R q = 1.
+__global__ void dd_assemble_kernel(int i0, int W, int fold, const double *rhon, const double *rhof, double tau,
+                                   double h2inv, double c, double *sd, double *se, double *sr) {
+    const int m = fold ? W / 2 : W;
+    const double s = tau * h2inv, f = fold ? 2.0 : 1.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int gi = i0 + i;
+        double dv = 1.0 + s * (rhof[gi] + rhof[gi + 1]) + tau * c * rhon[gi];
+        const double ev = -s * rhof[gi + 1];
+        if (fold && i == m - 1) dv += (fold == 1) ? ev : -ev;
+        sd[i] = f * dv;
+        se[i] = f * ev;
+        sr[i] = f * rhon[gi];
+    }
+}
+
+// Jacobi on C = R^{-1/2} S R^{-1/2} (symmetric tridiagonal) in shared memory; X = R^{-1/2} Z
+// (m x m, [i][a]) and, without refinement, theta and the mode pivots of modes moff + a.
+__global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int m, const double *sd, const double *se,
+                                                               const double *sr, double s, int W, int moff,
+                                                               double *Z, double *X, double *theta, double *idy,
+                                                               int sweeps, int pivots) {
     extern __shared__ double sh[];
+    const int Wf = W;
+    W = m;  // the Jacobi below runs on the m x m problem
     double *C = sh;                 // W x W (row stride W)
     double *cs = sh + W * W;        // rotation cos per pair
     double *sn = cs + DD_WMAX / 2 + 1;
@@ -193,16 +220,10 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, i
     // assemble C and Z = I
     for (int e = tid; e < W * W; e += blockDim.x) {
         const int r = e / W, k = e % W;
-        const int gi = i0 + r;  // 0-based node index
-        const double rr = rhon[gi];
         double v = 0.0;
-        if (r == k) {
-            v = (1.0 + tau * h2inv * (rhof[gi] + rhof[gi + 1]) + tau * c * rr) / rr;
-        } else if (k == r + 1) {
-            v = -tau * h2inv * rhof[gi + 1] / sqrt(rr * rhon[gi + 1]);
-        } else if (r == k + 1) {
-            v = -tau * h2inv * rhof[gi] / sqrt(rr * rhon[gi - 1]);
-        }
+        if (r == k) v = sd[r] / sr[r];
+        else if (k == r + 1) v = se[r] / sqrt(sr[r] * sr[k]);
+        else if (r == k + 1) v = se[k] / sqrt(sr[r] * sr[k]);
         C[e] = v;
         Z[e] = (r == k) ? 1.0 : 0.0;
     }
@@ -265,14 +286,12 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, i
             __syncthreads();
         }
     }
-    // eigenvalues on the diagonal; Q = R^{-1/2} Z; pivots of theta_a + 2 s, off -s (s = tau/h^2)
-    for (int a = tid; a < W; a += blockDim.x) dd_mode_pivots(n, W, a, DDd{C[a * W + a], 0.0}, tau * h2inv, theta, idy);
-    for (int e = tid; e < W * W; e += blockDim.x) {
-        const int r = e / W, k = e % W;
-        const double q = Z[e] / sqrt(rhon[i0 + r]);
-        Q[e] = q;             // Q[i][a]
-        QT[k * W + r] = q;    // QT[a][i]
-    }
+    // eigenvalues on the diagonal; X = R^{-1/2} Z; pivots of theta_a + 2 s, off -s (s = tau/h^2)
+    if (pivots)
+        for (int a = tid; a < W; a += blockDim.x) dd_mode_pivots(n, Wf, moff + a, DDd{C[a * W + a], 0.0}, s, theta, idy);
+    else
+        for (int a = tid; a < W; a += blockDim.x) Z[W * W + a] = C[a * W + a];  // theta for the refinement
+    for (int e = tid; e < W * W; e += blockDim.x) X[e] = Z[e] / sqrt(sr[e / W]);
 }
 
 // ------------------------------------------------ refinement of the eigenbasis ---
@@ -289,22 +308,23 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_factor_kernel(int n, int i0, i
 //     Q' = X (I + E),
 // after which Q'^T R Q' = I and Q'^T S Q' = Theta up to (eps ||C|| / gap)^2 and the rounding
 // of Q' itself.  One CTA per block, once per tau (setup).
-__global__ void __launch_bounds__(DD_FTHREADS) dd_refine_kernel(int n, int i0, int W, const double *rhon,
-                                                               const double *rhof, double tau, double h2inv,
-                                                               double c, double *scr, double *Q, double *QT,
-                                                               double *theta, double *idy) {
+__global__ void __launch_bounds__(DD_FTHREADS) dd_refine_kernel(int n, int m, const double *sd, const double *se,
+                                                               const double *sr, double s, int Wf, int moff,
+                                                               double *scr, double *X, double *theta,
+                                                               double *idy) {
     const int tid = threadIdx.x;
+    const int W = m;  // the m x m problem (dd_assemble_kernel)
     const int WW = W * W;
+    double *Q = X;
     double *Thi = scr, *Tlo = scr + WW, *Ms = scr + 2 * WW, *Mr = scr + 3 * WW;
     __shared__ double th[DD_WMAX], thl[DD_WMAX], dr[DD_WMAX];
-    const double s = tau * h2inv;
-    // T = S X (S tridiagonal, the block rows of I - tau A_j, dd.cuh header) in double-double
+    // T = S X (S tridiagonal) in double-double
     for (int e = tid; e < WW; e += blockDim.x) {
-        const int i = e / W, gi = i0 + i;
+        const int i = e / W;
         DDd t{0.0, 0.0};
-        dd_acc(t, 1.0 + s * (rhof[gi] + rhof[gi + 1]) + tau * c * rhon[gi], Q[e]);
-        if (i > 0) dd_acc(t, -s * rhof[gi], Q[e - W]);
-        if (i + 1 < W) dd_acc(t, -s * rhof[gi + 1], Q[e + W]);
+        dd_acc(t, sd[i], Q[e]);
+        if (i > 0) dd_acc(t, se[i - 1], Q[e - W]);
+        if (i + 1 < W) dd_acc(t, se[i], Q[e + W]);
         Thi[e] = t.hi;
         Tlo[e] = t.lo;
     }
@@ -318,8 +338,8 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_refine_kernel(int n, int i0, i
             const double xa = Q[i * W + a], xb = Q[i * W + b];
             dd_acc(ms, xa, Thi[i * W + b]);
             ms.lo = fma(xa, Tlo[i * W + b], ms.lo);
-            const double r = rhon[i0 + i];
-            const double pr = xa * r, pre = fma(xa, r, -pr);  // xa rho exactly = pr + pre
+            const double r = sr[i];
+            const double pr = xa * r, pre = fma(xa, r, -pr);  // xa r exactly = pr + pre
             dd_acc(mr, pr, xb);
             mr.lo = fma(pre, xb, mr.lo);
         }
@@ -347,7 +367,7 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_refine_kernel(int n, int i0, i
         Thi[e] = v;  // (T is dead)
     }
     __syncthreads();
-    // Q' = X + X E (the correction is ~1e-11 of X: fp64 suffices), into Tlo, then Q, QT
+    // X' = X + X E (the correction is ~1e-11 of X: fp64 suffices), into Tlo, then X
     for (int e = tid; e < WW; e += blockDim.x) {
         const int i = e / W, k = e % W;
         double corr = 0.0;
@@ -355,12 +375,22 @@ __global__ void __launch_bounds__(DD_FTHREADS) dd_refine_kernel(int n, int i0, i
         Tlo[e] = Q[e] + corr;
     }
     __syncthreads();
-    for (int e = tid; e < WW; e += blockDim.x) {
-        const int r = e / W, k = e % W;
-        Q[e] = Tlo[e];
-        QT[k * W + r] = Tlo[e];
+    for (int e = tid; e < WW; e += blockDim.x) Q[e] = Tlo[e];
+    for (int a = tid; a < W; a += blockDim.x) dd_mode_pivots(n, Wf, moff + a, DDd{th[a], thl[a]}, s, theta, idy);
+}
+
+// Q (W x W, [i][a]) and QT = Q^T of a block from the m x m X of one factorisation: fold 0: Q = X;
+// fold 1 (modes 0 .. m-1): Q[k][a] = X[k][a]; fold 2 (modes m .. W-1): Q[W-1-j][m+a] = X[j][a].
+// Positions k < W/2 of a folded tile hold F_k + F_{W-1-k}, positions W-1-j hold F_j - F_{W-1-j}
+// (dd_fold_tile), so G = T Q is [F_s U_s | F_a U_a]; the other entries stay zero (block
+// diagonal: the GEMM reads each n-tile's own block only).
+__global__ void dd_place_kernel(int W, int m, int fold, const double *X, double *Q, double *QT) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+        const int j = e / m, a = e % m;
+        const int row = (fold == 2) ? W - 1 - j : j, col = (fold == 2) ? m + a : a;
+        Q[row * W + col] = X[e];
+        QT[col * W + row] = X[e];
     }
-    for (int a = tid; a < W; a += blockDim.x) dd_mode_pivots(n, W, a, DDd{th[a], thl[a]}, s, theta, idy);
 }
 
 // ------------------------------------------------------------------ stage kernel ---
@@ -373,6 +403,7 @@ struct DDStageArgs {
     int CL, R;           // cluster size, rows per CTA
     int nblk;            // blocks of this colour
     const int *bi0, *bW; // block column start / width
+    const int *bWs;      // split stage: symmetric-half width of a folded block (dd_fold_tile), else W
     const double *const *Q, *const *QT, *const *idy;  // per block
     const double *const *conv;  // per block [W]: pivots of mode a are equal from this row on
     double tau, h2inv, c;
@@ -1127,8 +1158,12 @@ constexpr int DD2_THREADS = 32 * (DD_WMAX / 16);  // 9 warps
 constexpr int DD_SUB = DD_RMAX / 2;                // rows of a walk sub-piece (two per tile)
 static_assert(DD2_THREADS >= 2 * DD_WMAX, "two walking threads per mode");
 constexpr int DD2_PF = 3;
+// Ws < W (a folded block, see dd_fold_tile): M is block diagonal -- output columns c < Ws take
+// k < Ws only, columns >= Ws take k >= Ws -- so each 8-column n-tile runs over its own block's
+// k range (a warp whose two n-tiles lie in different blocks runs them one after the other).
 template <class SY>
-__device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restrict__ M, int W, int tid, SY sync) {
+__device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restrict__ M, int W, int Ws, int tid,
+                                              SY sync) {
     static_assert(DD_RMAX == 64 && DD_WMAX % 16 == 0, "dmma tiling of the split stage");
     const int lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fk = lane & 3, cb = 16 * warp;
@@ -1142,32 +1177,50 @@ __device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restric
     if (active) {
         const int c0 = cb + fr, c1 = cb + 8 + fr;
         const bool v0 = c0 < W, v1 = c1 < W;
-        const int nks = (W + 3) / 4;
-        double b0[DD2_PF], b1[DD2_PF];
-        auto ldb = [&](int ks, double &x0, double &x1) {
-            const int k = 4 * ks + fk;
-            const bool kin = k < W;
-            x0 = (kin && v0) ? __ldg(M + (long long)k * W + c0) : 0.0;
-            x1 = (kin && v1) ? __ldg(M + (long long)k * W + c1) : 0.0;
+        // k range of each n-tile (warp-uniform)
+        auto kr = [&](int cs, int &kb, int &ke) {
+            if (cs + 8 <= Ws) { kb = 0; ke = Ws; }
+            else if (cs >= Ws) { kb = Ws; ke = W; }
+            else { kb = 0; ke = W; }
         };
+        int kb0, ke0, kb1, ke1;
+        kr(cb, kb0, ke0);
+        kr(cb + 8, kb1, ke1);
+        // mask bit j: n-tile j accumulates in this run
+        auto run = [&](int kb, int ke, int mask) {
+            const int ks0 = kb >> 2, ks1 = (ke + 3) >> 2;
+            double b0[DD2_PF], b1[DD2_PF];
+            auto ldb = [&](int ks, double &x0, double &x1) {
+                const int k = 4 * ks + fk;
+                const bool kin = k < ke && k >= kb;
+                x0 = (kin && v0 && (mask & 1)) ? __ldg(M + (long long)k * W + c0) : 0.0;
+                x1 = (kin && v1 && (mask & 2)) ? __ldg(M + (long long)k * W + c1) : 0.0;
+            };
 #pragma unroll
-        for (int q = 0; q < DD2_PF; ++q) ldb(q, b0[q], b1[q]);
-        const double *ta = T + fk;
-        for (int ks0 = 0; ks0 < nks; ks0 += DD2_PF) {
+            for (int q = 0; q < DD2_PF; ++q) ldb(ks0 + q, b0[q], b1[q]);
+            const double *ta = T + fk;
+            for (int ksb = ks0; ksb < ks1; ksb += DD2_PF) {
 #pragma unroll
-            for (int q = 0; q < DD2_PF; ++q) {
-                const int ks = ks0 + q;
-                if (ks < nks) {
-                    const double bb0 = b0[q], bb1 = b1[q];
-                    ldb(ks + DD2_PF, b0[q], b1[q]);
+                for (int q = 0; q < DD2_PF; ++q) {
+                    const int ks = ksb + q;
+                    if (ks < ks1) {
+                        const double bb0 = b0[q], bb1 = b1[q];
+                        ldb(ks + DD2_PF, b0[q], b1[q]);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const double av = ta[cpad(8 * r + fr) * DD_WPAD + 4 * ks];
-                        dmma_f64(acc[r][0][0], acc[r][0][1], av, bb0);
-                        dmma_f64(acc[r][1][0], acc[r][1][1], av, bb1);
+                        for (int r = 0; r < 8; ++r) {
+                            const double av = ta[cpad(8 * r + fr) * DD_WPAD + 4 * ks];
+                            if (mask & 1) dmma_f64(acc[r][0][0], acc[r][0][1], av, bb0);
+                            if (mask & 2) dmma_f64(acc[r][1][0], acc[r][1][1], av, bb1);
+                        }
                     }
                 }
             }
+        };
+        if (kb0 == kb1 && ke0 == ke1) {
+            run(kb0, ke0, 3);
+        } else {
+            run(kb0, ke0, 1);
+            run(kb1, ke1, 2);
         }
     }
     sync();  // every read of the tile is done: write in place
@@ -1183,6 +1236,24 @@ __device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restric
             }
     }
     sync();
+}
+
+// Folded blocks (Ws = W / 2 < W: W even and rho bitwise mirror-symmetric over the block, so
+// S and R are centrosymmetric and every generalised eigenvector is symmetric or antisymmetric,
+// q = [u; +-J u]).  Then F Q = [F_s U_s | F_a U_a] with F_s,k = F_k + F_{W-1-k}, F_a,k =
+// F_k - F_{W-1-k} (k < W/2) and U_s / U_a the upper halves of the symmetric / antisymmetric
+// eigenvectors, and Q V^T unfolds the same way: half the GEMM flops.  In place, pairwise:
+// position k < W/2 takes the sum, position W-1-k the difference (the folded factors are laid
+// out to match, dd_place_kernel); the same pairwise map unfolds.
+__device__ __forceinline__ void dd_fold_tile(double *T, int W, int nrow, int tid, int nthreads) {
+    const int h = W >> 1;
+    for (int e = tid; e < nrow * h; e += nthreads) {
+        const int rl = e / h, k = e - rl * h;
+        double *row = T + cpad(rl) * DD_WPAD;
+        const double x = row[k], y = row[W - 1 - k];
+        row[k] = x + y;
+        row[W - 1 - k] = x - y;
+    }
 }
 
 // ------------------------------------------------------- split stage (default path) ----
@@ -1356,6 +1427,10 @@ struct DDTask {
 template <int DR, int SRC, class SY>
 __device__ __forceinline__ void dd_p1_pre(const DDStageArgs &a, double *T, const DDTask &t, int tid, SY sync) {
     dd_load_tile<DR, SRC, DD2_THREADS>(a, T, t.b, t.blk, t.r0, t.nrow, tid, sync);
+    if (a.bWs[t.blk] < t.W) {
+        sync();
+        dd_fold_tile(T, t.W, t.nrow, tid, DD2_THREADS);
+    }
 }
 // pass 1 after its GEMM: G to global (bulk copies by one thread while the walks read the tile),
 // the piece's transfer tuples; the tile is free again when this returns
@@ -1429,6 +1504,10 @@ __device__ __forceinline__ void dd_p2_post(const DDStageArgs &a, double *T, cons
             if (ci < t.W && (a.stage == 1 || !(rn_ot[i0 + ci] > 0.0))) finm |= 1u << k;
         }
     }
+    if (a.bWs[t.blk] < t.W) {  // the GEMM's sync published the tile
+        dd_fold_tile(T, t.W, t.nrow, tid, DD2_THREADS);
+        sync();
+    }
     dd_store_tile<DR, DD2_THREADS>(a, T, t.b, t.blk, t.r0, t.nrow, finm, tid);
     sync();
 }
@@ -1455,7 +1534,7 @@ __global__ void __launch_bounds__(DD2_THREADS, 2) dd_pass_kernel(DDStageArgs a) 
 #ifdef PRS_DD_TIMING
     if (!(a.abl & 1))
 #endif
-    dd_tile_gemm2(T, (PASS == 1 ? a.Q : a.QT)[t.blk], t.W, tid, sy);
+    dd_tile_gemm2(T, (PASS == 1 ? a.Q : a.QT)[t.blk], t.W, a.bWs[t.blk], tid, sy);
     DD2T(PASS == 1 ? 1 : 4);
     if (PASS == 1) dd_p1_post(a, T, t, tid, sy, wp);
     else dd_p2_post<DR>(a, T, t, tid, sy);
@@ -1525,8 +1604,9 @@ struct DDData {
     double c = 0, h2inv = 0;
     double *rhon = nullptr, *rhof = nullptr, *Z = nullptr;  // Z: Jacobi eigenvectors + refinement scratch
     bool refine = true;  // Newton refinement of the eigenbasis (PRS_DDREFINE=0: Jacobi only)
-    std::vector<int> bi0[2], bW[2];
-    int *d_bi0[2] = {nullptr, nullptr}, *d_bW[2] = {nullptr, nullptr};
+    std::vector<int> bi0[2], bW[2], bWs[2];  // bWs: W / 2 for a folded block (dd_fold_tile), else W
+    int *d_bi0[2] = {nullptr, nullptr}, *d_bW[2] = {nullptr, nullptr}, *d_bWs[2] = {nullptr, nullptr};
+    bool fold = true;  // split stage: mirror-symmetric even blocks folded (PRS_DDFOLD=0: never)
     // per tau slot (3) and colour (2): device arrays of per-block pointers + the storage
     double tau[3] = {-1.0, -1.0, -1.0};
     std::vector<double *> store[3];
@@ -1616,7 +1696,7 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     }
     if (cudaMalloc(&d.rhon, sizeof(double) * 2 * d.n) != cudaSuccess ||
         cudaMalloc(&d.rhof, sizeof(double) * 2 * (d.n + 1)) != cudaSuccess ||
-        cudaMalloc(&d.Z, sizeof(double) * 5 * DD_WMAX * DD_WMAX) != cudaSuccess) {
+        cudaMalloc(&d.Z, sizeof(double) * (7 * DD_WMAX * DD_WMAX + 3 * DD_WMAX)) != cudaSuccess) {
         err = "cudaMalloc (DD tables) failed";
         return PRS_ECUDA;
     }
@@ -1650,6 +1730,32 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
     d.dfpart = !(dpv && dpv[0] == '0');
     const char *rfv = getenv("PRS_DDREFINE");
     d.refine = !(rfv && rfv[0] == '0');
+    const char *fdv = getenv("PRS_DDFOLD");
+    d.fold = d.split && !d.full && !(fdv && fdv[0] == '0');
+    {
+        // folded blocks: W even, rho_j bitwise mirror-symmetric over the block's nodes and faces
+        std::vector<double> hn(2 * d.n), hf(2 * (d.n + 1));
+        cudaMemcpyAsync(hn.data(), d.rhon, sizeof(double) * hn.size(), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(hf.data(), d.rhof, sizeof(double) * hf.size(), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        for (int col = 0; col < 2; ++col) {
+            const size_t nb = d.bi0[col].size();
+            d.bWs[col].assign(nb, 0);
+            for (size_t k = 0; k < nb; ++k) {
+                const int i0 = d.bi0[col][k], W = d.bW[col][k];
+                bool sym = d.fold && (W % 2 == 0);
+                for (int q = 0; sym && q < W; ++q) sym = hn[col * d.n + i0 + q] == hn[col * d.n + i0 + W - 1 - q];
+                for (int q = 0; sym && q <= W; ++q)
+                    sym = hf[col * (d.n + 1) + i0 + q] == hf[col * (d.n + 1) + i0 + W - q];
+                d.bWs[col][k] = sym ? W / 2 : W;
+            }
+            if (cudaMalloc(&d.d_bWs[col], sizeof(int) * nb) != cudaSuccess) {
+                err = "cudaMalloc (DD blocks) failed";
+                return PRS_ECUDA;
+            }
+            cudaMemcpyAsync(d.d_bWs[col], d.bWs[col].data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st);
+        }
+    }
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1775,13 +1881,26 @@ inline int dd_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
                 return PRS_ECUDA;
             }
             d.store[slot].insert(d.store[slot].end(), {Q, QT, th, idy});
-            dd_factor_kernel<<<1, DD_FTHREADS, fsm, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
-                                                         d.rhof + col * (d.n + 1), tau, d.h2inv, d.c, d.Z, Q, QT,
-                                                         th, idy, 14);
-            if (d.refine)
-                dd_refine_kernel<<<1, DD_FTHREADS, 0, st>>>(d.n, d.bi0[col][k], W, d.rhon + col * d.n,
-                                                            d.rhof + col * (d.n + 1), tau, d.h2inv, d.c,
-                                                            d.Z + DD_WMAX * DD_WMAX, Q, QT, th, idy);
+            // one factorisation per block, or two (symmetric / antisymmetric half) per folded block
+            const bool fold = d.bWs[col][k] < W;
+            if (fold) {
+                cudaMemsetAsync(Q, 0, sizeof(double) * W * W, st);
+                cudaMemsetAsync(QT, 0, sizeof(double) * W * W, st);
+            }
+            constexpr size_t WW2 = (size_t)DD_WMAX * DD_WMAX;
+            double *Zb = d.Z, *Xb = d.Z + 2 * WW2, *scr = d.Z + 3 * WW2;
+            double *sd = d.Z + 7 * WW2, *se = sd + DD_WMAX, *sr = se + DD_WMAX;
+            for (int f = fold ? 1 : 0; f <= (fold ? 2 : 0); ++f) {
+                const int m = f ? W / 2 : W, moff = (f == 2) ? m : 0;
+                dd_assemble_kernel<<<1, 256, 0, st>>>(d.bi0[col][k], W, f, d.rhon + col * d.n,
+                                                      d.rhof + col * (d.n + 1), tau, d.h2inv, d.c, sd, se, sr);
+                dd_factor_kernel<<<1, DD_FTHREADS, fsm, st>>>(d.n, m, sd, se, sr, tau * d.h2inv, W, moff, Zb, Xb, th,
+                                                             idy, 14, d.refine ? 0 : 1);
+                if (d.refine)
+                    dd_refine_kernel<<<1, DD_FTHREADS, 0, st>>>(d.n, m, sd, se, sr, tau * d.h2inv, W, moff, scr, Xb,
+                                                                th, idy);
+                dd_place_kernel<<<64, 256, 0, st>>>(W, m, f, Xb, Q, QT);
+            }
             hQ[k] = Q;
             hQT[k] = QT;
             hI[k] = idy;
@@ -1828,10 +1947,23 @@ inline void dd_free(DDData &d) {
     for (int c = 0; c < 2; ++c) {
         if (d.d_bi0[c]) cudaFree(d.d_bi0[c]);
         if (d.d_bW[c]) cudaFree(d.d_bW[c]);
+        if (d.d_bWs[c]) cudaFree(d.d_bWs[c]);
     }
 }
 
 // one DD step (two colour stages) on B states: in -> out
+// algorithmic fp64 flops of one split-stage colour per state: per support point of a W-wide
+// block two W x W transforms (2 W each) and the tridiagonal solve along y (~10); a folded block
+// (dd_fold_tile) does two W/2 x W/2 transforms per half (2 W in all) plus the fold / unfold (2)
+inline double dd_split_flops(const DDData &d, int stage) {
+    double flops = 0.0;
+    for (size_t k = 0; k < d.bW[stage].size(); ++k) {
+        const double w = d.bW[stage][k];
+        flops += w * d.n * ((d.bWs[stage][k] < d.bW[stage][k]) ? (2.0 * w + 12.0) : (4.0 * w + 10.0));
+    }
+    return flops;
+}
+
 inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, double *out, long long B,
                         const TimeArgs &ta, int epi, const double *gc, double *gcache, const double *delta,
                         double *traj, unsigned long long *red, cudaStream_t st, prs_ctx *prof, std::string &err,
@@ -1877,9 +2009,7 @@ inline int dd_step(DDData &d, int scheme, int slot, const double *in, double *ou
         return PRS_ECUDA;
     }
     if (prof) {
-        double flops = 0.0;
-        for (int stage = 0; stage < 2; ++stage)
-            for (int w : d.bW[stage]) flops += (double)w * d.n * (4.0 * w + 10.0);
+        const double flops = dd_split_flops(d, 0) + dd_split_flops(d, 1);
         // both colour stages of the step in one interval: accounted as two stage launches
         if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
     }
@@ -2051,6 +2181,7 @@ inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, doubl
         a.nblk = (int)d.bi0[stage].size();
         a.bi0 = d.d_bi0[stage];
         a.bW = d.d_bW[stage];
+        a.bWs = d.d_bWs[stage];
         a.Q = d.d_Q[slot][stage];
         a.QT = d.d_QT[slot][stage];
         a.idy = d.d_idy[slot][stage];
@@ -2133,11 +2264,8 @@ inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, doubl
                     return PRS_ECUDA;
                 }
             }
-            if (prof) {
-                double flops = 0.0;
-                for (int w : d.bW[stage]) flops += (double)w * n * (4.0 * w + 10.0);
-                if (prs_internal_prof_end(prof, PRS_K_DD, (double)B * flops) != PRS_OK) return PRS_ECUDA;
-            }
+            if (prof && prs_internal_prof_end(prof, PRS_K_DD, (double)B * dd_split_flops(d, stage)) != PRS_OK)
+                return PRS_ECUDA;
             continue;
         }
         if (d.gx && ntasks > d.gcap) {

@@ -177,6 +177,33 @@ DD_STEP_CASES = [
 ]
 
 
+@pytest.mark.parametrize("p", [DD_STEP_CASES[0], DD_STEP_CASES[2], DD_STEP_CASES[3], synth.CONFIGS["c4"]],
+                         ids=lambda p: f"n{p.n}_S{p.dd_strips}_b{p.dd_overlap}")
+def test_dd_folded_blocks_match_unfolded(p, monkeypatch):
+    """Mirror-symmetric even blocks (linear ramps) are folded into symmetric / antisymmetric
+    halves (dd.cuh dd_fold_tile: half the GEMM flops, factorised as two half problems): the
+    folded split stage agrees with the unfolded one (PRS_DDFOLD=0) to rounding, FIE and DR,
+    coarse and fine tau, and differs from it bitwise (the fold did run)."""
+    prs = prs_mod()
+    u = synth.initial_state(p.replace(init="modes", seed=3))
+    du = dev(u)
+    outs = []
+    for fold in ("1", "0"):
+        monkeypatch.setenv("PRS_DDFOLD", fold)
+        ctx = prs.Context(p)
+        res = []
+        for sch in (FIE, DR):
+            for tau in (p.T / (p.N * p.s), p.T / p.N):
+                out = torch.empty_like(du)
+                ctx.step(sch, tau, 2 * tau, du, out)
+                res.append(host(out).copy())
+        ctx.close()
+        outs.append(res)
+    for a, b in zip(*outs):
+        assert nerr(a, b, b, u) <= 1e-13
+    assert any(not np.array_equal(a, b) for a, b in zip(*outs))
+
+
 @pytest.mark.parametrize("exchange", ["split", "l2", "cluster"])
 @pytest.mark.parametrize("p", DD_STEP_CASES, ids=lambda p: f"n{p.n}_S{p.dd_strips}_b{p.dd_overlap}_r{p.dd_ramp}")
 def test_dd_single_step_parity(p, exchange, monkeypatch):
@@ -799,6 +826,12 @@ def test_twin_iterates_match_stored_oracle_digests(name):
     # on both GPU DD stage forms (the oracle's own FMA-contracted build: 2e-12,
     # tests/golden/twins/c4r_DR-DR_floor.json); the bar is 2e-11 there, 1e-11 elsewhere
     tol = 2e-11 if p.G == DR and p.split == 1 else TOL
+    # DESIGN.md R28: at c4's full size the ORACLE's band elimination is 2.4e-13 of |U| off the
+    # extended-precision value per fine step (the GPU's refined eigenbasis 5e-15; test above) and
+    # drifts ~2e-11 over one slice's 64 fine steps (scripts/xprec_c4_fine.py), so from k = 1 on
+    # the stored c4_k1 iterate itself carries several 1e-11 of oracle rounding: held at 1e-10
+    # there, k = 0 (the coarse chain, oracle drift < 1e-13) at 1e-11
+    tol_k1 = 1e-10 if name == "c4_k1" else tol
     signs = synth.projection_signs(p.npts)
     prs = prs_mod()
     u0 = synth.initial_state(p)
@@ -818,12 +851,13 @@ def test_twin_iterates_match_stored_oracle_digests(name):
         es = float(np.max(np.abs(g["samples"] - d["samples"][k]))) / scale
         ep = float(np.max(np.abs(g["proj"] - d["proj"][k]))) / (scale * math.sqrt(p.npts))
         ei = float(np.max(np.abs(g["inf"] - d["inf"][k]))) / scale
-        assert es <= tol and ep <= tol and ei <= tol, (k, es, ep, ei)
+        tk = tol if k == 0 else tol_k1
+        assert es <= tk and ep <= tk and ei <= tk, (k, es, ep, ei)
     ctx.close()
     cupds = d["upd"]
     for k in range(K):
         sc = max(1.0, float(np.max(d["inf"][: k + 2])) / scale0)
-        assert abs(gupds[k] - cupds[k]) <= tol * sc, (k, gupds[k], cupds[k])
+        assert abs(gupds[k] - cupds[k]) <= tol_k1 * sc, (k, gupds[k], cupds[k])
     if meta["tol"] > 0.0:  # the GPU stops at the same k under the same rule (R7)
         assert all(u > meta["tol"] for u in gupds[:-1]) and (gupds[-1] <= meta["tol"] or K == p.N)
 
@@ -894,13 +928,16 @@ def test_long_line_rounding_floor_at_large_tau():
     assert e_gpu <= 2.0 * e_cpu + 1e-14, (e_gpu, e_cpu)
 
 
-def test_c4_full_size_dd_coarse_step_against_extended_precision():
-    """c4's coarse step (1024^2, 8 strips, 8-cell overlap, tau = Delta T = 1/32: tau / h^2 =
-    3.3e4) from c4's smooth initial state, against the extended-precision step (tests/xprec.py):
-    the GPU's eigenbasis block solve must be as accurate as the oracle's band elimination
-    (within twice its distance from the exact value, R23 / R28).  Before the Newton
-    refinement of the eigenbasis (dd.cuh dd_refine_kernel) the GPU was 7e-12 of |U| off, the
-    oracle 2e-13 -- enough for c4's 32 coarse steps to drift 3.5e-11 from the oracle."""
+@pytest.mark.parametrize("which", ["coarse", "fine"])
+def test_c4_full_size_dd_step_against_extended_precision(which):
+    """c4's coarse (tau = Delta T = 1/32: tau / h^2 = 3.3e4) and fine (tau = delta t = 1/2048)
+    step at full size (1024^2, 8 strips, 8-cell overlap) from c4's smooth initial state, against
+    the extended-precision step (tests/xprec.py).  The GPU's eigenbasis block solve must be as
+    accurate as the oracle's band elimination (within twice its distance from the exact value,
+    DESIGN.md R23), and -- since the refined eigenbasis and double-double mode pivots (DESIGN.md
+    R28) -- within 1e-13 of it (measured 2.8e-15 / 5e-15; the oracle 2.1e-13 / 2.4e-13).
+    Before that refinement the GPU's coarse step was 7e-12 of |U| off -- enough for c4's 32
+    coarse steps to drift 3.5e-11 from the oracle."""
     from tests.xprec import XStep
     p = synth.CONFIGS["c4"]
     prs = prs_mod()
@@ -908,16 +945,16 @@ def test_c4_full_size_dd_coarse_step_against_extended_precision():
     u = synth.initial_state(p)
     du = dev(u)
     out = torch.empty_like(du)
-    dT = p.T / p.N
-    ctx.step(FIE, dT, dT, du, out)
+    tau = p.T / p.N if which == "coarse" else p.T / (p.N * p.s)
+    ctx.step(FIE, tau, tau, du, out)
     ctx.close()
-    ref, _ = XStep(p).step(FIE, dT, dT, u)
-    want = oracle.Oracle(p).step(FIE, dT, dT, u)
+    ref, _ = XStep(p).step(FIE, tau, tau, u)
+    want = oracle.Oracle(p).step(FIE, tau, tau, u)
     nref = float(np.max(np.abs(ref)))
     e_cpu = float(np.max(np.abs(want.astype(np.longdouble) - ref))) / nref
     e_gpu = float(np.max(np.abs(host(out).astype(np.longdouble) - ref))) / nref
-    print(f"c4 coarse step vs extended precision: oracle {e_cpu:.3e}, GPU {e_gpu:.3e} (of |U_n+1|)")
-    assert e_gpu <= 2.0 * e_cpu + 1e-14, (e_gpu, e_cpu)
+    print(f"c4 {which} step vs extended precision: oracle {e_cpu:.3e}, GPU {e_gpu:.3e} (of |U_n+1|)")
+    assert e_gpu <= 2.0 * e_cpu + 1e-14 and e_gpu <= 1e-13, (e_gpu, e_cpu)
 
 
 # ------------------------------------------ NEXT-3: the full diffusion tensor (section 5.2)
