@@ -1158,16 +1158,32 @@ constexpr int DD2_THREADS = 32 * (DD_WMAX / 16);  // 9 warps
 constexpr int DD_SUB = DD_RMAX / 2;                // rows of a walk sub-piece (two per tile)
 static_assert(DD2_THREADS >= 2 * DD_WMAX, "two walking threads per mode");
 constexpr int DD2_PF = 3;
-// Ws < W (a folded block, see dd_fold_tile): M is block diagonal -- output columns c < Ws take
-// k < Ws only, columns >= Ws take k >= Ws -- so each 8-column n-tile runs over its own block's
-// k range (a warp whose two n-tiles lie in different blocks runs them one after the other).
 template <class SY>
 __device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restrict__ M, int W, int Ws, int tid,
                                               SY sync) {
     static_assert(DD_RMAX == 64 && DD_WMAX % 16 == 0, "dmma tiling of the split stage");
     const int lane = tid & 31, warp = tid >> 5;
-    const int fr = lane >> 2, fk = lane & 3, cb = 16 * warp;
-    const bool active = cb < W;  // warp-uniform
+    const int fr = lane >> 2, fk = lane & 3;
+    // the warp's two 8-column n-tiles: 2 warp and 2 warp + 1, except on a folded block whose
+    // halves meet inside an n-tile (Ws % 8 != 0, e.g. c4's W = 136): that n-tile needs both
+    // halves' k ranges (twice the k-steps), so it stays alone in its warp and its partner moves
+    // to the last warp's free slot (an odd n-tile count), which keeps the warps balanced
+    const int ntiles = (W + 7) >> 3;
+    int nt0 = 2 * warp, nt1 = 2 * warp + 1;
+    {
+        const int ns = (Ws < W && (Ws & 7)) ? (Ws >> 3) : -1, wl = (ntiles - 1) >> 1;
+        if (ns >= 0 && (ntiles & 1) && (ns >> 1) != wl) {
+            if (warp == (ns >> 1)) {
+                nt0 = ns;
+                nt1 = -1;
+            } else if (warp == wl) {
+                nt1 = ns ^ 1;
+            }
+        }
+    }
+    if (nt0 >= ntiles) nt0 = -1;
+    if (nt1 >= ntiles) nt1 = -1;
+    const bool active = nt0 >= 0;  // warp-uniform
     double acc[8][2][2];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -1175,17 +1191,20 @@ __device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restric
         for (int c = 0; c < 2; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
     sync();  // the tile is complete
     if (active) {
-        const int c0 = cb + fr, c1 = cb + 8 + fr;
-        const bool v0 = c0 < W, v1 = c1 < W;
-        // k range of each n-tile (warp-uniform)
-        auto kr = [&](int cs, int &kb, int &ke) {
-            if (cs + 8 <= Ws) { kb = 0; ke = Ws; }
+        const int c0 = 8 * nt0 + fr, c1 = 8 * nt1 + fr;
+        const bool v0 = c0 < W, v1 = nt1 >= 0 && c1 < W;
+        // k range of each n-tile (warp-uniform): Ws < W (a folded block, see dd_fold_tile): M is
+        // block diagonal -- output columns c < Ws take k < Ws only, columns >= Ws take k >= Ws
+        auto kr = [&](int nt, int &kb, int &ke) {
+            const int cs = 8 * nt;
+            if (nt < 0) { kb = ke = 0; }
+            else if (cs + 8 <= Ws) { kb = 0; ke = Ws; }
             else if (cs >= Ws) { kb = Ws; ke = W; }
             else { kb = 0; ke = W; }
         };
         int kb0, ke0, kb1, ke1;
-        kr(cb, kb0, ke0);
-        kr(cb + 8, kb1, ke1);
+        kr(nt0, kb0, ke0);
+        kr(nt1, kb1, ke1);
         // mask bit j: n-tile j accumulates in this run
         auto run = [&](int kb, int ke, int mask) {
             const int ks0 = kb >> 2, ks1 = (ke + 3) >> 2;
@@ -1216,7 +1235,9 @@ __device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restric
                 }
             }
         };
-        if (kb0 == kb1 && ke0 == ke1) {
+        if (nt1 < 0) {
+            run(kb0, ke0, 1);
+        } else if (kb0 == kb1 && ke0 == ke1) {
             run(kb0, ke0, 3);
         } else {
             run(kb0, ke0, 1);
@@ -1229,7 +1250,9 @@ __device__ __forceinline__ void dd_tile_gemm2(double *T, const double *__restric
         for (int r = 0; r < 8; ++r)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int col = cb + 8 * c + 2 * fk;
+                const int nt = c ? nt1 : nt0;
+                if (nt < 0) continue;
+                const int col = 8 * nt + 2 * fk;
                 double *p = T + cpad(8 * r + fr) * DD_WPAD + col;
                 if (col < W) p[0] = acc[r][c][0];
                 if (col + 1 < W) p[1] = acc[r][c][1];
