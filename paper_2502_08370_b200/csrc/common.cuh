@@ -138,7 +138,7 @@ __device__ __forceinline__ void walk_b3(double *sp, int cnt, const V &v, double 
 #pragma unroll
     for (int i = LCH - 1; i >= 0; --i)
         if (FULL || i < cnt) {
-            x = fma(v.ID(i), sp[i], -v.CC(i) * x);
+            x = fma(-v.CC(i), x, v.ID(i) * sp[i]);
             sp[i] = x;
         }
 }

@@ -1096,7 +1096,7 @@ __device__ __forceinline__ void dd_stage_task(const DDStageArgs &a, double *sh, 
                 const double id = __ldg(ip + (long long)i * W);
                 const double ccv = (lb + i == n - 1) ? 0.0 : ms * id;
                 double *p = T + cpad(e0 + i) * DD_WPAD + am;
-                x = fma(id, *p, -ccv * x);
+                x = fma(-ccv, x, id * *p);
                 *p = x;
             }
     };
@@ -1422,7 +1422,7 @@ __device__ __forceinline__ void dd_piece_walks(const DDStageArgs &a, double *T, 
             for (int i = 0; i < U; ++i) {
                 const int l = r0 + c1 - i;
                 const double ccv = (l == n - 1) ? 0.0 : ms * id[i];
-                x = fma(id[i], t[i], -ccv * x);
+                x = fma(-ccv, x, id[i] * t[i]);
                 t[i] = x;
             }
 #pragma unroll

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(L3T, 1) lpass3_kernel(L3Args a) {
         // B3
 #pragma unroll
         for (int i = LCH - 1; i >= 0; --i) {
-            x = fma(ci(i), v[i], -cc(i) * x);
+            x = fma(-cc(i), x, ci(i) * v[i]);
             v[i] = x;
         }
         // ---- store from registers + fused epilogue ----

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(L3T, 1) lpass4_kernel(L3Args a) {
         double x = X;
 #pragma unroll
         for (int i = LCH - 1; i >= 0; --i) {
-            x = fma(ci(c, i), v[i], -cc(c, i) * x);
+            x = fma(-cc(c, i), x, ci(c, i) * v[i]);
             v[i] = x;
         }
         const long long g0 = panel_base(p) + (long long)gr0 * a.Sl + w;

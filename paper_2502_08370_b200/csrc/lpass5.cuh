@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(L5T, 2) lp5_finish_kernel(L5Args a) {
     double x = X;
 #pragma unroll
     for (int i = LCH - 1; i >= 0; --i) {
-        x = fma(c.ci(i), c.v[i], -c.cc(i) * x);
+        x = fma(-c.cc(i), x, c.ci(i) * c.v[i]);
         c.v[i] = x;
     }
     // ---- store + fused epilogue ----

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(L5T, L8Cfg<WIDE>::MINB) lp8_kernel(L5Args a) {
             double x = X;
 #pragma unroll
             for (int i = LCH - 1; i >= 0; --i) {
-                x = fma(c.ci(i), c.v[i], -c.cc(i) * x);
+                x = fma(-c.cc(i), x, c.ci(i) * c.v[i]);
                 c.v[i] = x;
             }
             const long long g0 = b * a.vol + (long long)r0 * n + col;

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
             double x = EQ;
 #pragma unroll
             for (int i = LCH - 1; i >= 0; --i) {
-                x = fma(ti[i], v[i], -tc[i] * x);
+                x = fma(-tc[i], x, ti[i] * v[i]);
                 p[i] = DR ? x - w[k][i] : x;
             }
         }
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(SW_T, 2) sweep2_kernel(SWArgs a) {
             double x = X;
 #pragma unroll
             for (int i = LCH - 1; i >= 0; --i) {
-                x = fma(yi(t, i), p[i * S], -yc(t, i) * x);
+                x = fma(-yc(t, i), x, yi(t, i) * p[i * S]);
                 p[i * S] = x;
             }
         }

@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ 
         double x = fma(EP, Xw, EQ);
 #pragma unroll
         for (int i = LCH - 1; i >= 0; --i) {
-            x = fma(cid(i), v[i], -ccc(i) * x);
+            x = fma(-ccc(i), x, cid(i) * v[i]);
             v[i] = DR ? x - w[i] : x;
         }
         __syncthreads();  // every read of ib(g) / scr done

@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(const __grid_constant__ 
             double x = fma(EP, Xw, EQ);
 #pragma unroll
             for (int i = LCH - 1; i >= 0; --i) {
-                x = fma(cid(i), v[i], -ccc(i) * x);
+                x = fma(-ccc(i), x, cid(i) * v[i]);  // one fma on the chain (cid v off it)
                 v[i] = DR ? x - w[i] : x;
             }
 #ifdef PRS_X7_DIRECT

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
             double x = EQ;  // x leaving the chunk (x after the row's end = 0)
 #pragma unroll
             for (int i = LCH - 1; i >= 0; --i) {
-                x = fma(ti[i], v[i], -tcv(i) * x);
+                x = fma(-tcv(i), x, ti[i] * v[i]);
                 v[i] = x;
             }
 #pragma unroll
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
         double x = X;
 #pragma unroll
         for (int i = LCH - 1; i >= 0; --i) {
-            x = fma(yi(t, i), v[i], -yc(t, i) * x);
+            x = fma(-yc(t, i), x, yi(t, i) * v[i]);
             v[i] = x;
         }
         double *p = tile + (t * LCH) * XY_S + cpad(w);
