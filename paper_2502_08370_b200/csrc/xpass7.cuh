@@ -401,7 +401,10 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(const __grid_constant__ 
             __syncthreads();  // every read of ib(g), scr and xin is done before the slots are refilled
 #else
             if (TMA) {
-                __syncthreads();  // every read of ib(g), scr and xin is done
+                // no barrier before the staging writes: the staging slot ib(g) held row g's pivots,
+                // read into registers before this row's first barrier; the scratch totals of the
+                // next row are written only after the barrier below, which every warp reaches past
+                // its reads of this row's totals
                 double *dst = ib(g);
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
