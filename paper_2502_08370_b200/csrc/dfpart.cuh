@@ -467,10 +467,21 @@ __global__ void __launch_bounds__(DFP_T, 1) dfp_bwd_kernel(DFPArgs x) {
             yr[j] = (MODE != 2 && e < W * DFP_S && l >= 0) ? x.ys[(t.bg * n + l) * DF_WMAX * DFP_S + e] : 0.0;
         }
     };
+    // the y-face coefficient d(x_i, y_{l+3/2}) of C_l's diagonal, a row ahead like y (an L2 load
+    // per element and row: on the critical path it was the kernel's top stall)
+    double dyr[DFP_RPT];
+    auto ldd = [&](int l) {
+#pragma unroll
+        for (int j = 0; j < DFP_RPT; ++j) {
+            const int e = threadIdx.x + j * DFP_T;
+            dyr[j] = (e < W * DFP_S && l >= 0 && l < n - 1) ? x.op_me.dyf[(long long)(l + 1) * n + t.i0 + e / DFP_S] : 0.0;
+        }
+    };
     ldy(t.a + t.m - 1);
+    ldd(t.a + t.m - 1);
     for (int rl = t.m - 1; rl >= 0; --rl) {
         const int l = t.a + rl;
-        // T = y_l - C_l x_{l+1}  (C = -tau (coefficients of row l + 1))
+        // T = y_l - C_l x_{l+1}  (C = -tau (coefficients of row l + 1), DFOp::up)
 #pragma unroll
         for (int j = 0; j < DFP_RPT; ++j) {
             const int e = threadIdx.x + j * DFP_T;
@@ -478,8 +489,10 @@ __global__ void __launch_bounds__(DFP_T, 1) dfp_bwd_kernel(DFPArgs x) {
             const int i = e / DFP_S, s = e % DFP_S;
             double v = yr[j];
             if (l < n - 1) {
-                double cm, c0, cp;
-                x.op_me.up(t.i0 + i, l, cm, c0, cp);
+                const int gi = t.i0 + i;
+                const double rxm = x.op_me.rhof[gi], rxp = x.op_me.rhof[gi + 1], rn = x.op_me.rhon[gi];
+                const double h2i = x.op_me.h2inv;
+                const double c0 = rn * dyr[j] * h2i, cp = rxp * 0.125 * h2i, cm = -rxm * 0.125 * h2i;
                 double sx = c0 * Xc[i * DFP_SP + s];
                 if (i > 0) sx = fma(cm, Xc[(i - 1) * DFP_SP + s], sx);
                 if (i + 1 < W) sx = fma(cp, Xc[(i + 1) * DFP_SP + s], sx);
@@ -488,7 +501,10 @@ __global__ void __launch_bounds__(DFP_T, 1) dfp_bwd_kernel(DFPArgs x) {
             Tt[i * DFP_SP + s] = v;
         }
         __syncthreads();
-        if (rl > 0) ldy(l - 1);
+        if (rl > 0) {
+            ldy(l - 1);
+            ldd(l - 1);
+        }
         // x_l = P_l^{-1} T_l into Xc (x_{l+1} is dead)
         dfp_rowstep_s(st, PI + l * WW, rl > 0 ? PI + (l - 1) * WW : nullptr, W, Tt, Xc, 1.0, true);
         if (MODE == 1) {

@@ -14,5 +14,5 @@ cap lp8t c3 "lp8_kernel" 300
 cap lp8f c3 "lp8_kernel" 301
 cap ddp1 c4 "dd_pass_kernel" 140
 cap ddp2 c4 "dd_pass_kernel" 141
-cap dfpf c5 "dfp_fwd" 130
-cap dfpb c5 "dfp_bwd" 131
+cap dfpf c5 "dfp_fwd" 400
+cap dfpb c5 "dfp_bwd" 401
