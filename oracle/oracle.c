@@ -14,6 +14,8 @@
  *   - FIE step           : PAPER.md:151-157 (eq. FIE_method).
  *   - DR step            : PAPER.md:165-171 (eq. DR_method), predictor (I + tau A)U_n
  *                          evaluated literally with the unsplit A (reading R1).
+ *   - IE step            : unsplit implicit Euler, the Parareal/IE-IE baseline (PAPER.md:455,
+ *                          SPEC.md:206-214), band elimination of the whole system (NEXT-4).
  *   - stage solves       : Thomas per grid line (dimensional, "one-dimensional
  *                          uncoupled systems"), band Gaussian elimination per strip block
  *                          (DD, "q independent subsystems"); factorised on the fly.
@@ -484,9 +486,68 @@ static void dr_step(const orc_problem *p, double tau, double t_next, const doubl
     free(prev); free(F); free(Au); free(rhs);
 }
 
-/* one step of scheme (0 FIE, 1 DR) of size tau; the source is sampled at t_next = t_{n+1} */
+/* Unsplit implicit Euler (the Parareal/IE-IE baseline of PAPER.md:455):
+ *   (I - tau A) U_{n+1} = U_n + tau F_{n+1},  A the unsplit operator (term -1).
+ * Plain band Gaussian elimination (no pivoting: I - tau A is an M-matrix, diagonally dominant)
+ * of the whole n^dim system in node order, half bandwidth n (2-D 5-point), n + 1 (2-D 9-point
+ * full tensor) or n^2 (3-D 7-point); factorised on the fly.  O(n^dim bw^2): tiny grids only. */
+static void ie_step(const orc_problem *p, double tau, double t_next, const double *u, double *out) {
+    int n = p->n, nz = (p->dim == 3) ? n : 1;
+    long Nb = npoints(p), sy = n, sz = (long)n * n;
+    long bw = (p->dim == 3) ? sz : (p->coef == 2 ? n + 1 : n);
+    long ld = 2 * bw + 1;
+    double *Ab = calloc((size_t)(Nb * ld), sizeof(double));
+    double *F = malloc(sizeof(double) * Nb);
+    double row[11];
+    orc_source(p, t_next, F);
+    for (long k = 0; k < Nb; ++k) out[k] = u[k] + tau * F[k];
+    for (int m = 1; m <= nz; ++m)
+        for (int l = 1; l <= n; ++l)
+            for (int i = 1; i <= n; ++i) {
+                long q = node_index(p, i, l, m);
+                orc_row(p, -1, i, l, m, row);
+                Ab[q * ld + bw] = 1.0 - tau * row[0];
+                if (i > 1) Ab[q * ld + bw - 1] = -tau * row[1];
+                if (i < n) Ab[q * ld + bw + 1] = -tau * row[2];
+                if (l > 1) Ab[q * ld + bw - sy] = -tau * row[3];
+                if (l < n) Ab[q * ld + bw + sy] = -tau * row[4];
+                if (p->dim == 3) {
+                    if (m > 1) Ab[q * ld + bw - sz] = -tau * row[5];
+                    if (m < n) Ab[q * ld + bw + sz] = -tau * row[6];
+                }
+                if (p->coef == 2) {
+                    if (i > 1 && l > 1) Ab[q * ld + bw - sy - 1] = -tau * row[7];
+                    if (i < n && l > 1) Ab[q * ld + bw - sy + 1] = -tau * row[8];
+                    if (i > 1 && l < n) Ab[q * ld + bw + sy - 1] = -tau * row[9];
+                    if (i < n && l < n) Ab[q * ld + bw + sy + 1] = -tau * row[10];
+                }
+            }
+    /* forward elimination */
+    for (long k = 0; k < Nb; ++k) {
+        double piv = Ab[k * ld + bw];
+        long iend = k + bw < Nb - 1 ? k + bw : Nb - 1;
+        for (long q = k + 1; q <= iend; ++q) {
+            double f = Ab[q * ld + (k - q + bw)] / piv;
+            if (f == 0.0) continue;
+            for (long c = k; c <= iend; ++c) Ab[q * ld + (c - q + bw)] -= f * Ab[k * ld + (c - k + bw)];
+            out[q] -= f * out[k];
+        }
+    }
+    /* back substitution */
+    for (long k = Nb - 1; k >= 0; --k) {
+        double s = out[k];
+        long cend = k + bw < Nb - 1 ? k + bw : Nb - 1;
+        for (long c = k + 1; c <= cend; ++c) s -= Ab[k * ld + (c - k + bw)] * out[c];
+        out[k] = s / Ab[k * ld + bw];
+    }
+    free(Ab);
+    free(F);
+}
+
+/* one step of scheme (0 FIE, 1 DR, 2 IE) of size tau; the source is sampled at t_next = t_{n+1} */
 void orc_step(const orc_problem *p, int scheme, double tau, double t_next, const double *u, double *out) {
-    if (scheme == 1) dr_step(p, tau, t_next, u, out);
+    if (scheme == 2) ie_step(p, tau, t_next, u, out);
+    else if (scheme == 1) dr_step(p, tau, t_next, u, out);
     else fie_step(p, tau, t_next, u, out);
 }
 

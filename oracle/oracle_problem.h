@@ -18,7 +18,7 @@ typedef struct {
     double T;       /* final time                                                      */
     int N;          /* coarse slices N_c                                               */
     int s;          /* fine steps per slice                                            */
-    int G, F;       /* scheme of the coarse / fine propagator: 0 FIE, 1 DR            */
+    int G, F;       /* scheme of the coarse / fine propagator: 0 FIE, 1 DR, 2 IE      */
 } orc_problem;
 
 #endif

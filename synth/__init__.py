@@ -17,8 +17,8 @@ import math
 
 import numpy as np
 
-FIE, DR = 0, 1
-SCHEME = {"FIE": FIE, "DR": DR}
+FIE, DR, IE = 0, 1, 2  # IE: unsplit implicit Euler (Parareal/IE-IE baseline, NEXT-4)
+SCHEME = {"FIE": FIE, "DR": DR, "IE": IE}
 
 
 @dataclasses.dataclass
@@ -52,7 +52,7 @@ class Problem:
         return dataclasses.replace(self, **kw)
 
     def label(self) -> str:
-        names = {FIE: "FIE", DR: "DR"}
+        names = {FIE: "FIE", DR: "DR", IE: "IE"}
         sp = "dd" if self.split else "dim"
         return f"{self.dim}d_n{self.n}_{sp}_{names[self.G]}-{names[self.F]}_N{self.N}_s{self.s}"
 

@@ -8,6 +8,7 @@
 * Scalar (per-mode) FIE / DR steps with a source amplitude b(t) on the mode:
       FIE: v = a + tau b(t_{n+1});  v <- v / (1 - z_j), j = 1..M       (eq. FIE_method)
       DR : v = (1 + sum z) a + tau b;  v <- (v - z_j a) / (1 - z_j)    (eq. DR_method)
+      IE : v = (a + tau b) / (1 - sum z)                               (unsplit)
   and scalar parareal on them.
 """
 from __future__ import annotations
@@ -49,6 +50,8 @@ def conv_factor(zs, s, G="FIE", F="FIE"):
 
 def scalar_step(scheme, a, lam, tau, b):
     zs = [tau * l for l in lam]
+    if scheme == 2:  # IE, unsplit: (1 - sum z) v = a + tau b
+        return (a + tau * b) / (1 - sum(zs))
     if scheme == 0:  # FIE
         v = a + tau * b
         for z in zs:
