@@ -76,7 +76,7 @@ def updates_per_step(p) -> int:
 
 
 def workload_config(p, name, n_gpus):
-    sch = {0: "FIE", 1: "DR"}
+    sch = {0: "FIE", 1: "DR", 2: "IE"}
     kap = {0: "1", 1: "1+0.5sin2pix sin2piy", 2: "full tensor d11=d22=1/(2+cos3pix cos2piy), d12=1/4"}[p.coef]
     return {"workload": name, "grid": f"{p.n}^{p.dim}", "kappa": kap,
             "split": "dd" if p.split else "dimensional", "pairing": f"{sch[p.G]}-{sch[p.F]}",
@@ -371,7 +371,7 @@ def run_prs(args):
     for _ in range(args.steps):
         step()
     torch.cuda.synchronize()
-    stats = {k: ctx.kernel_stats(k) for k in (prs.PRS_K_XPASS, prs.PRS_K_LPASS, prs.PRS_K_DD)}
+    stats = {k: ctx.kernel_stats(k) for k in (prs.PRS_K_XPASS, prs.PRS_K_LPASS, prs.PRS_K_DD, prs.PRS_K_IE)}
     ctx.set_profiling(False)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -441,11 +441,13 @@ def run_prs(args):
     nl, kms, kwork = stats[dom]
     names = {prs.PRS_K_XPASS: "xpass_kernel (x-line solve + fused RHS)",
              prs.PRS_K_LPASS: "lpass_kernel (strided line solve + epilogue)",
-             prs.PRS_K_DD: "dd_stage_kernel (DD strip-block stage)"}
+             prs.PRS_K_DD: "dd_stage_kernel (DD strip-block stage)",
+             prs.PRS_K_IE: "ie_axis_kernel (unsplit IE step: 2 dim sine transforms on DMMA)"}
+    flop_kinds = (prs.PRS_K_DD, prs.PRS_K_IE)
     tr = ncu_traffic(args.config)
     per_launch_s = (kms / nl) / 1e3 if nl else float("nan")
-    if dom == prs.PRS_K_DD:
-        # the block transforms run on the fp64 tensor cores (DMMA m8n8k4); fp64 peak = 148 SMs x
+    if dom in flop_kinds:
+        # the block / sine transforms run on the fp64 tensor cores (DMMA m8n8k4); fp64 peak = 148 SMs x
         # 64 FP64 FMA/clk x 2 flop x 1.965 GHz = 37.2 TF/s, DMMA and DFMA alike (measured 37.1 /
         # 35.7 TF/s on this pool's B200, profiles/r01_fp64_peak_probe.txt)
         peak, peak_src, unit, bound = (148 * 64 * 2 * 1.965e9 / 1e12,
@@ -461,7 +463,7 @@ def run_prs(args):
         if not v[0]:
             return None
         r = (v[2] / v[0]) / ((v[1] / v[0]) / 1e3)
-        return r / 1e12 if v is stats.get(prs.PRS_K_DD) else r / 1e9
+        return r / 1e12 if any(v is stats.get(k) for k in flop_kinds) else r / 1e9
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": (tr or {}).get(names[dom].split()[0]),
             "kernel": names[dom], "peak_source": peak_src,
@@ -469,10 +471,16 @@ def run_prs(args):
             "avg_launch_ms": kms / nl if nl else None,
             "share_of_step": kms / ms if ms else None,
             "other_kernels": {names[k]: {"launches": v[0], "ms": v[1],
-                                         ("TFLOPs" if k == prs.PRS_K_DD else "GBps"): rate(v)}
+                                         ("TFLOPs" if k in flop_kinds else "GBps"): rate(v)}
                               for k, v in stats.items() if v[0]}}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    ie_big = (p.G == 2 or p.F == 2) and p.n > 300
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and ie_big:
+        # the oracle's IE step is a band elimination of the whole n^2 system, O(n^4) per step
+        # (~10^12 flops, minutes, at n = 999): no bounded sample of this workload exists
+        cpu = {"kind": "oracle", "skipped": "oracle IE step is O(n^4) band elimination: one step of "
+               f"n = {p.n} exceeds the bounded-sample budget", "cores": 0, "value": None}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         reps = oracle_reps_for(p)
         v, sec, meta = oracle_sample(p, reps)
         meta.update({"value": v, "unit": UNIT, "seconds": sec})

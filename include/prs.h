@@ -36,6 +36,10 @@ extern "C" {
 
 #define PRS_FIE 0
 #define PRS_DR 1
+#define PRS_IE 2  /* unsplit implicit Euler (I - tau A) U' = U + tau F(t'): the Parareal/IE-IE
+                     baseline of PAPER.md:455.  GPU path:
+                     constant coefficients only (coef_kind 0; solved exactly in the sine basis,
+                     ie.cuh); any other coef_kind returns PRS_EUNSUPPORTED from prs_create */
 
 typedef struct prs_ctx prs_ctx;
 
@@ -45,8 +49,7 @@ typedef struct prs_problem {
     int n;            /* interior nodes per axis (>= 1)                                  */
     double c;         /* reaction coefficient, L u = div(kappa grad u) - c u */
     int coef_kind;    /* 0: kappa = 1;  1: kappa = 1 + 0.5 sin(2 pi x) sin(2 pi y) (2-D);
-                         2: the full tensor of PAPER.md:523-528 (NEXT-3) -- PRS_EUNSUPPORTED
-                            on the GPU path for now (the CPU oracle implements it) */
+                         2: the full tensor of PAPER.md:523-528 (NEXT-3; 2-D DD split only) */
     int split;        /* 0: dimensional, M = dim;  1: domain decomposition, M = 2 (2-D)  */
     int dd_strips;    /* DD: number of vertical strips 2q (n % dd_strips == 0)           */
     int dd_overlap;   /* DD: overlap width in cells (even, < n/dd_strips)                */
@@ -55,8 +58,8 @@ typedef struct prs_problem {
     double T;         /* final time                                                      */
     int N;            /* coarse slices N_c, Delta T = T/N                  */
     int s;            /* fine steps per slice, delta t = Delta T / s                     */
-    int G;            /* coarse scheme PRS_FIE / PRS_DR                                  */
-    int F;            /* fine scheme   PRS_FIE / PRS_DR                                  */
+    int G;            /* coarse scheme PRS_FIE / PRS_DR / PRS_IE                         */
+    int F;            /* fine scheme   PRS_FIE / PRS_DR / PRS_IE                         */
 } prs_problem;
 
 /* Create a context.  Validates the problem before allocating (PRS_EINVAL), allocates the
@@ -115,8 +118,9 @@ int prs_iterate(prs_ctx *ctx, int kmax, double tol, int *k_out, double *hist);
  * (PRS_EINVAL elsewhere; see prs_set_ownership for cyclic ownership). */
 int prs_get_slice(prs_ctx *ctx, int n, double *out, int out_on_device);
 
-/* One FIE/DR step of size tau from a device state `in` to device `out` (in != out), the
- * source sampled at t_next = t_{n+1}.  Test hook for per-step parity. */
+/* One FIE/DR/IE step of size tau from a device state `in` to device `out` (in != out), the
+ * source sampled at t_next = t_{n+1} (SPEC.md:211 for IE).  Test hook for
+ * per-step parity.  PRS_IE needs a context created with G or F = PRS_IE (its sine tables). */
 int prs_step(prs_ctx *ctx, int scheme, double tau, double t_next, const double *in, double *out);
 
 /* One step of the coarse (which = 0: tau = Delta T, source at (slice0 + b + 1) Delta T) or the
@@ -187,13 +191,16 @@ int prs_gpar_plan(int N, int nranks, int rank, int phase, int *ops, int max_ops)
 /* Counters.  prs_launches: kernels this context has launched so far.  With profiling on,
  * every fine-sweep kernel launch is bracketed by CUDA events on the context stream and
  * prs_kernel_stats(kind) returns, for kind PRS_K_XPASS (contiguous-axis line solve),
- * PRS_K_LPASS (strided-axis line solve) or PRS_K_DD (DD strip-block stage), the launch
+ * PRS_K_LPASS (strided-axis line solve), PRS_K_DD (DD strip-block stage) or PRS_K_IE (one
+ * unsplit IE step: 2 dim sine-transform launches, bracketed together), the launch
  * count, the summed device time (ms, synchronises) and the summed ALGORITHMIC work: bytes
  * (state read + state write + precomputed factors read) for the line passes,
- * fp64 flops for PRS_K_DD (two W x W transforms + the y solve per support point). */
+ * fp64 flops for PRS_K_DD (two W x W transforms + the y solve per support point) and for
+ * PRS_K_IE (4 dim n flops per point). */
 #define PRS_K_XPASS 0
 #define PRS_K_LPASS 1
 #define PRS_K_DD 2
+#define PRS_K_IE 3  /* unsplit IE step (sine transforms on DMMA): fp64 flops */
 int prs_set_profiling(prs_ctx *ctx, int on);
 long long prs_launches(const prs_ctx *ctx);
 int prs_kernel_stats(prs_ctx *ctx, int kind, long long *launches, double *ms, double *bytes);

@@ -16,8 +16,8 @@ import os
 from ._build import SO, build  # noqa: F401
 
 PRS_OK, PRS_EINVAL, PRS_EDIVERGED, PRS_EUNSUPPORTED, PRS_ECUDA, PRS_ENCCL = 0, 2, 3, 4, 5, 6
-PRS_FIE, PRS_DR = 0, 1
-PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD = 0, 1, 2
+PRS_FIE, PRS_DR, PRS_IE = 0, 1, 2
+PRS_K_XPASS, PRS_K_LPASS, PRS_K_DD, PRS_K_IE = 0, 1, 2, 3
 EXPORTS = ["prs_create", "prs_nccl_unique_id", "prs_partition", "prs_set_initial",
            "prs_coarse_sweep", "prs_fine_sweep", "prs_parareal_correct", "prs_iterate",
            "prs_get_slice", "prs_step", "prs_step_batch", "prs_fine_solve", "prs_set_coarse_mode", "prs_set_pipeline", "prs_gpar_plan", "prs_set_profiling", "prs_launches", "prs_kernel_stats",

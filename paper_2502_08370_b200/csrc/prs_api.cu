@@ -30,6 +30,7 @@
 #include "sweep2.cuh"
 #include "xpass7.cuh"
 #include "transport.cuh"
+#include "ie.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -172,8 +173,12 @@ struct prs_ctx {
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, double>> ev_pending;  // (kind, bytes) per recorded pair
     size_t ev_used = 0;
-    long long k_launch[3] = {0, 0, 0};
-    double k_ms[3] = {0, 0, 0}, k_bytes[3] = {0, 0, 0};
+    long long k_launch[4] = {0, 0, 0, 0};
+    double k_ms[4] = {0, 0, 0, 0}, k_bytes[4] = {0, 0, 0, 0};
+    // unsplit implicit Euler (ie.cuh, NEXT-4): DST-I matrix, sine eigenvalues, two scratch
+    // batches of ie_cap states (grown on demand: scratch_gen++)
+    double *ie_S = nullptr, *ie_mu = nullptr, *ie_w1 = nullptr, *ie_w2 = nullptr;
+    long long ie_cap = 0;
     Transport *tr = nullptr;  // nranks > 1: NCCL (prs_create) or the in-process world (prs_create_local)
     int num_sms = 148;
     bool no_xy = false;        // PRS_XY=0: 3-D n = 128 takes separate x and y passes
@@ -304,6 +309,8 @@ static int ensure_factors(prs_ctx *ctx, int slot, double tau) {
     if (f.tau == tau) return PRS_OK;
     const int n = ctx->p.n;
     f.tau = tau;
+    // an IE propagator solves in the sine basis (ie.cuh): no splitting factors for its slot
+    if ((slot == 0 && ctx->p.G == PRS_IE) || (slot == 1 && ctx->p.F == PRS_IE)) return PRS_OK;
     if (ctx->p.split == 1) return dd_factors(ctx->dd, slot, tau, ctx->stream, ctx->err);
     if (ctx->p.coef_kind == 0) {
         if (!f.tab) CK(cudaMalloc(&f.tab, sizeof(double) * 3 * n));
@@ -804,8 +811,17 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
 
 // One step of `scheme` on B consecutive states: in -> out (out holds the result, or the
 // epilogue consumes it).  tmp must be distinct from in when scheme is DR.
+static int ie_step(prs_ctx *ctx, double tau, const double *in, double *out, long long B, const TimeArgs &ta,
+                   const EpiArgs &ep, bool prof);
 static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
                     long long B, const TimeArgs &ta, const EpiArgs &ep, bool prof, long long stride) {
+    if (scheme == PRS_IE) {
+        if (stride != ctx->vol) {
+            ctx->err = "internal: padded slice stride on the IE path";
+            return PRS_EUNSUPPORTED;
+        }
+        return ie_step(ctx, f.tau, in, out, B, ta, ep, prof);
+    }
     if (ctx->p.split == 1)
         return dd_step(ctx->dd, scheme, (int)(&f - ctx->fac), in, out, B, ta, ep.kind, ep.gc, ep.gcache,
                        ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err, ctx->launches,
@@ -853,6 +869,69 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
     EpiArgs st;
     TRY(launch_lpass(ctx, 1, f, out, out, B, st, prof));
     return launch_lpass(ctx, 2, f, out, out, B, ep, prof);
+}
+
+// One unsplit implicit-Euler step (ie.cuh) on B consecutive states: dim forward sine transforms
+// (the first forms U + tau F on its loads, the last divides by 1 + tau (c + sum mu) and
+// normalises), dim inverse transforms (the last carries the epilogue).  Scratch alternates
+// between two batches, so `in` may alias `out`.
+static int ie_step(prs_ctx *ctx, double tau, const double *in, double *out, long long B, const TimeArgs &ta,
+                   const EpiArgs &ep, bool prof) {
+    const int n = ctx->p.n, dim = ctx->p.dim;
+    if (B > ctx->ie_cap) {
+        if (ctx->ie_w1) CK(cudaFree(ctx->ie_w1));
+        if (ctx->ie_w2) CK(cudaFree(ctx->ie_w2));
+        ctx->ie_w1 = ctx->ie_w2 = nullptr;
+        ctx->ie_cap = 0;
+        const long long cap = std::max<long long>(B, ctx->count);
+        CK(cudaMalloc(&ctx->ie_w1, ctx->sbytes * cap));
+        CK(cudaMalloc(&ctx->ie_w2, ctx->sbytes * cap));
+        ctx->ie_cap = cap;
+        ctx->scratch_gen++;  // captured graphs hold the old scratch pointers
+    }
+    IEArgs a{};
+    a.S = ctx->ie_S;
+    a.mu = ctx->ie_mu;
+    a.vol = ctx->vol;
+    a.ncols = B * (ctx->vol / n);
+    a.n = n;
+    a.dim = dim;
+    a.src = ctx->p.source_kind;
+    a.tau = tau;
+    a.src_amp = (double)dim * M_PI * M_PI + ctx->p.c - 1.0;
+    a.sinpi = ctx->sinpi;
+    a.ta = ta;
+    a.creact = ctx->p.c;
+    a.norm = std::pow(2.0 / (double)(n + 1), dim);
+    a.e_gc = ep.gc;
+    a.e_gcache = ep.gcache;
+    a.e_delta = ep.delta;
+    a.e_traj = ep.traj;
+    a.e_red = ctx->red;
+    const dim3 grid((unsigned)((a.ncols + IE_BN - 1) / IE_BN), (unsigned)((n + IE_BM - 1) / IE_BM));
+    double *w[2] = {ctx->ie_w1, ctx->ie_w2};
+    const double *src = in;
+    if (prof) TRY(prof_begin(ctx));
+    for (int pass = 0; pass < 2 * dim; ++pass) {
+        const int axis = pass % dim;
+        const bool last = pass == 2 * dim - 1;
+        a.in = src;
+        a.out = last ? out : w[pass & 1];
+        a.inner = 1;
+        for (int d = 0; d < axis; ++d) a.inner *= n;
+        if (pass == 0) ie_axis_kernel<1, EPI_STORE><<<grid, IE_T, 0, ctx->stream>>>(a);
+        else if (pass == dim - 1) ie_axis_kernel<0, IE_SCALE><<<grid, IE_T, 0, ctx->stream>>>(a);
+        else if (!last) ie_axis_kernel<0, EPI_STORE><<<grid, IE_T, 0, ctx->stream>>>(a);
+        else if (ep.kind == EPI_DELTA) ie_axis_kernel<0, EPI_DELTA><<<grid, IE_T, 0, ctx->stream>>>(a);
+        else if (ep.kind == EPI_CORRECT) ie_axis_kernel<0, EPI_CORRECT><<<grid, IE_T, 0, ctx->stream>>>(a);
+        else if (ep.kind == EPI_INIT) ie_axis_kernel<0, EPI_INIT><<<grid, IE_T, 0, ctx->stream>>>(a);
+        else ie_axis_kernel<0, EPI_STORE><<<grid, IE_T, 0, ctx->stream>>>(a);
+        TRY(last_launch(ctx));
+        src = a.out;
+    }
+    // fp64 flops: 2 dim transforms, each n multiply-adds per output element
+    if (prof) TRY(prof_end(ctx, PRS_K_IE, 2.0 * dim * 2.0 * n * (double)B * (double)ctx->vol));
+    return PRS_OK;
 }
 
 // hook for dd.cuh profiling
@@ -905,9 +984,15 @@ static int validate(const prs_problem *p, std::string &err) {
     if (p->n < 1) { err = "n must be >= 1"; return PRS_EINVAL; }
     if (!(p->c >= 0.0) || !(p->T > 0.0)) { err = "need c >= 0 and T > 0"; return PRS_EINVAL; }
     if (p->N < 1 || p->s < 1) { err = "need N >= 1 and s >= 1"; return PRS_EINVAL; }
-    if ((p->G != PRS_FIE && p->G != PRS_DR) || (p->F != PRS_FIE && p->F != PRS_DR)) {
-        err = "schemes must be PRS_FIE or PRS_DR";
+    if ((p->G != PRS_FIE && p->G != PRS_DR && p->G != PRS_IE) ||
+        (p->F != PRS_FIE && p->F != PRS_DR && p->F != PRS_IE)) {
+        err = "schemes must be PRS_FIE, PRS_DR or PRS_IE";
         return PRS_EINVAL;
+    }
+    if ((p->G == PRS_IE || p->F == PRS_IE) && p->coef_kind != 0) {
+        err = "the unsplit implicit Euler (PRS_IE) solves in the sine basis: constant coefficients "
+              "(coef_kind 0, the paper's D = I problem of PAPER.md:449) only on the GPU path";
+        return PRS_EUNSUPPORTED;
     }
     if (p->coef_kind == 2 && (p->split != 1 || p->dim != 2)) {
         err = "the full diffusion tensor (coef_kind 2, PAPER.md:520-546) needs the 2-D DD split (mixed "
@@ -1023,6 +1108,14 @@ static int create_impl(const prs_problem *prob, int rank, int nranks, Transport 
             return drc;
         }
         ctx->dd.sinpi = ctx->sinpi;
+    }
+    if (prob->G == PRS_IE || prob->F == PRS_IE) {
+        CKC(cudaMalloc(&ctx->ie_S, sizeof(double) * (size_t)n * n));
+        CKC(cudaMalloc(&ctx->ie_mu, sizeof(double) * n));
+        const long long ne = (long long)n * n;
+        ie_setup_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, ctx->stream>>>(n, ctx->h2inv, ctx->ie_S, ctx->ie_mu);
+        ctx->launches++;
+        CKC(cudaGetLastError());
     }
     int frc = ensure_factors(ctx, 0, ctx->dT);
     if (frc == PRS_OK) frc = ensure_factors(ctx, 1, ctx->dt);
@@ -1168,6 +1261,8 @@ void prs_destroy(prs_ctx *ctx) {
     if (ctx->l5buf) cudaFree(ctx->l5buf);
     if (ctx->fine_exec) cudaGraphExecDestroy(ctx->fine_exec);
     {
+        for (double *q : {ctx->ie_S, ctx->ie_mu, ctx->ie_w1, ctx->ie_w2})
+            if (q) cudaFree(q);
         double *gb[] = {ctx->gb_u, ctx->gb_d, ctx->gb_gc, ctx->gb_v, ctx->gb_tt, ctx->gb_tot, ctx->gb_yx};
         for (double *b : gb)
             if (b) cudaFree(b);
@@ -1272,6 +1367,7 @@ static int local_start(const prs_ctx *ctx) {
 static bool sweep2_ok(const prs_ctx *ctx) {
     const int n = ctx->p.n;
     return !ctx->no_sweep2 && ctx->p.dim == 2 && ctx->p.split == 0 && ctx->p.coef_kind == 0 &&
+           ctx->p.G != PRS_IE && ctx->p.F != PRS_IE &&
            (n == 32 || n == 64 || n == 128 || n == 256);
 }
 
@@ -2035,8 +2131,23 @@ int prs_get_slice(prs_ctx *ctx, int n, double *out, int out_on_device) {
 
 int prs_step(prs_ctx *ctx, int scheme, double tau, double t_next, const double *in, double *out) {
     if (!ctx || !in || !out || in == out || !(tau > 0.0)) return PRS_EINVAL;
-    if (scheme != PRS_FIE && scheme != PRS_DR) return PRS_EINVAL;
+    if (scheme != PRS_FIE && scheme != PRS_DR && scheme != PRS_IE) return PRS_EINVAL;
     if (ctx->p.dim == 3 && scheme == PRS_DR) return PRS_EUNSUPPORTED;
+    if (scheme == PRS_IE && !ctx->ie_S) {
+        ctx->err = "PRS_IE steps need a context created with G or F = PRS_IE";
+        return PRS_EINVAL;
+    }
+    if (scheme == PRS_IE) {
+        TimeArgs ta;
+        ta.slice0 = 0;
+        ta.tmul = 0;
+        ta.toff = 1;
+        ta.tstep = t_next;
+        EpiArgs ep;
+        TRY(ie_step(ctx, tau, in, out, 1, ta, ep, false));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return PRS_OK;
+    }
     int slot = 2;
     if (tau == ctx->fac[0].tau) slot = 0;
     else if (tau == ctx->fac[1].tau) slot = 1;
@@ -2201,7 +2312,7 @@ int prs_set_ownership(prs_ctx *ctx, int mode) {
 int prs_set_profiling(prs_ctx *ctx, int on) {
     if (!ctx) return PRS_EINVAL;
     ctx->prof = on != 0;
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 4; ++k) {
         ctx->k_launch[k] = 0;
         ctx->k_ms[k] = 0;
         ctx->k_bytes[k] = 0;
@@ -2212,7 +2323,7 @@ int prs_set_profiling(prs_ctx *ctx, int on) {
 long long prs_launches(const prs_ctx *ctx) { return ctx ? ctx->launches : -1; }
 
 int prs_kernel_stats(prs_ctx *ctx, int kind, long long *launches, double *ms, double *bytes) {
-    if (!ctx || kind < 0 || kind > 2) return PRS_EINVAL;
+    if (!ctx || kind < 0 || kind > 3) return PRS_EINVAL;
     TRY(prof_flush(ctx));
     if (launches) *launches = ctx->k_launch[kind];
     if (ms) *ms = ctx->k_ms[kind];

@@ -79,6 +79,11 @@ CONFIGS = {
     # (d11 = d22 = 1/(2 + cos 3pi x cos 2pi y), d12 = 1/4), the paper's Parareal/FIE-FIE
     "c5": Problem(dim=2, n=1024, c=1.0, coef=2, split=1, dd_strips=8, dd_overlap=8, dd_ramp=0,
                   source=1, N=32, s=64, G=FIE, F=FIE, init="phi"),
+    # c6: the Parareal/IE-IE baseline on the grid of the paper's
+    # section-5.1 experiments: h = 1e-3 (n = 999), T = 1, Delta T = 0.05
+    # (N = 20), delta t = 2.5e-3 (s = 20), D = I, c = 0; the manufactured e^{-t} sin sin source
+    # stands in for the paper's sin(2 pi t) sin(2 pi x) sin(2 pi y) solution (R29)
+    "c6": Problem(dim=2, n=999, c=0.0, source=1, N=20, s=20, G=IE, F=IE, init="phi"),
 }
 
 
