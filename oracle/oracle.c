@@ -309,6 +309,18 @@ void orc_dense(const orc_problem *p, int term, double *Mat) {
  * f = (dim pi^2 + c - 1) e^{-t} prod_d sin(pi x_d)  (BASELINE c0/c2/c4). */
 void orc_source(const orc_problem *p, double t, double *F) {
     long N = npoints(p);
+    if (p->source == 2) {
+        /* source == 2 (2-D, D = I): the solution u = sin(2 pi t) sin(2 pi x) sin(2 pi y) of the
+         * section-5.1 experiments, f = u_t - Delta u + c u
+         *   = (2 pi cos(2 pi t) + (8 pi^2 + c) sin(2 pi t)) sin(2 pi x) sin(2 pi y) */
+        int n = p->n;
+        double h = grid_h(p);
+        double amp = 2.0 * ORC_PI * cos(2.0 * ORC_PI * t) + (8.0 * ORC_PI * ORC_PI + p->c) * sin(2.0 * ORC_PI * t);
+        for (int l = 1; l <= n; ++l)
+            for (int i = 1; i <= n; ++i)
+                F[node_index(p, i, l, 1)] = amp * sin(2.0 * ORC_PI * i * h) * sin(2.0 * ORC_PI * l * h);
+        return;
+    }
     if (p->source != 1) {
         for (long k = 0; k < N; ++k) F[k] = 0.0;
         return;

@@ -14,7 +14,8 @@ typedef struct {
     int dd_strips;  /* DD: total number of vertical strips (2q)           */
     int dd_overlap; /* DD: overlap width beta in cells                                 */
     int dd_ramp;    /* DD: 0 linear ramp, 1 cosine ramp                                */
-    int source;     /* 0: f = 0;  1: manufactured f for u = e^{-t} prod sin(pi x_d)    */
+    int source;     /* 0: f = 0;  1: manufactured f for u = e^{-t} prod sin(pi x_d);   */
+                    /* 2: f for u = sin(2 pi t) sin(2 pi x) sin(2 pi y) (2-D, D = I) */
     double T;       /* final time                                                      */
     int N;          /* coarse slices N_c                                               */
     int s;          /* fine steps per slice                                            */

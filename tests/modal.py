@@ -66,12 +66,15 @@ def scalar_step(scheme, a, lam, tau, b):
 class ScalarParareal:
     """Parareal on one eigen-mode: amplitude recurrences in mpmath."""
 
-    def __init__(self, lam, T, N, s, G, F, src_amp=0.0):
+    def __init__(self, lam, T, N, s, G, F, src_amp=0.0, bfun=None):
         self.lam = lam
         self.T, self.N, self.s, self.G, self.F = mp.mpf(T), N, s, G, F
         self.src_amp = mp.mpf(src_amp)
+        self.bfun = bfun  # source amplitude b(t) on the mode (default src_amp e^{-t})
 
     def b(self, t):
+        if self.bfun is not None:
+            return self.bfun(t)
         return self.src_amp * mp.exp(-t)
 
     def coarse(self, n, a):

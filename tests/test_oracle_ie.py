@@ -111,3 +111,45 @@ def test_ie_ie_finite_termination_variable_kappa():
         assert nrm_err(trajs[p.N][n], fine[n], scale) <= 1e-14
     # and not earlier: the k = 1 iterate is still off at the last slice
     assert nrm_err(trajs[1][p.N], fine[p.N], scale) > 1e-8
+
+
+# ------------------------------------------ the section-5.1 problem (source 2, R29)
+def _u51(t, x, y):
+    return mp.sin(2 * mp.pi * t) * mp.sin(2 * mp.pi * x) * mp.sin(2 * mp.pi * y)
+
+
+def test_section51_source_is_ut_minus_laplacian_plus_cu():
+    """F = u_t - (u_xx + u_yy) + c u for u = sin(2 pi t) sin(2 pi x) sin(2 pi y) (PAPER.md:444-449,
+    D = I), the derivatives taken numerically by mpmath at sample nodes and times"""
+    p = Problem(dim=2, n=9, c=0.7, source=2)
+    o = oracle.Oracle(p)
+    h = 1.0 / (p.n + 1)
+    for t in (0.0, 0.13, 0.5, 0.91):
+        F = o.source(t)
+        for i, l in ((1, 1), (3, 7), (9, 4)):
+            x, y = i * h, l * h
+            want = (mp.diff(lambda s: _u51(s, x, y), t) - mp.diff(lambda s: _u51(t, s, y), x, 2)
+                    - mp.diff(lambda s: _u51(t, x, s), y, 2) + p.c * _u51(t, x, y))
+            assert abs(F[l - 1, i - 1] - float(want)) <= 1e-12 * 100, (t, i, l)
+
+
+@pytest.mark.parametrize("G,F", [(IE, IE), (FIE, DR), (FIE, FIE)])
+def test_section51_parareal_modal_closed_form(G, F):
+    """P1 with the section-5.1 source: u0 = 0 and F on mode (2, 2) only, so every iterate is
+    a^k_n sin(2 pi x) sin(2 pi y) with the scalar recurrence driven by
+    b(t) = 2 pi cos(2 pi t) + (8 pi^2 + c) sin(2 pi t)"""
+    c = 0.0
+    p = Problem(dim=2, n=14, c=c, source=2, N=5, s=4, G=G, F=F, init="zero")
+    o = oracle.Oracle(p)
+    u0 = synth.initial_state(p)
+    trajs, _ = o.parareal(u0, p.N, fixed=True)
+    lam = modal.lambdas((2, 2), p.n, p.c, 2)
+    sp = modal.ScalarParareal(lam, p.T, p.N, p.s, G, F,
+                              bfun=lambda t: 2 * mp.pi * mp.cos(2 * mp.pi * t)
+                              + (8 * mp.pi ** 2 + c) * mp.sin(2 * mp.pi * t))
+    want = sp.run(0, p.N)
+    shape = mode_shape(p.n, (2, 2))
+    scale = max(np.max(np.abs(t)) for t in trajs)
+    for k in range(p.N + 1):
+        for n in range(p.N + 1):
+            assert nrm_err(trajs[k][n], float(want[k][n]) * shape, scale) <= 1e-13, (k, n)
