@@ -74,9 +74,19 @@ struct TimeArgs {
     long long slice0 = 0, tmul = 0, toff = 0;
     double tstep = 0.0;
     long long sstride = 1;
+    int gk = 0;        // source time factor: 0 e^{-t} (source_kind 1), 1 the section-5.1 solution's
+    double gc = 0.0;   // (source_kind 2): 2 pi cos(2 pi t) + gc sin(2 pi t), gc = 8 pi^2 + c
 };
 __device__ __forceinline__ double src_time(const TimeArgs &ta, long long b) {
     return (double)((ta.slice0 + b * ta.sstride) * ta.tmul + ta.toff) * ta.tstep;
+}
+// time factor of the source of state b (times src_amp and the spatial sine product):
+// source_kind 1: f = (dim pi^2 + c - 1) e^{-t} prod sin(pi x_d)  (u = e^{-t} prod sin(pi x_d));
+// source_kind 2: f = (2 pi cos 2 pi t + (8 pi^2 + c) sin 2 pi t) sin(2 pi x) sin(2 pi y), the
+// solution u = sin(2 pi t) sin(2 pi x) sin(2 pi y) of PAPER.md:444-445 with D = I (src_amp = 1)
+__device__ __forceinline__ double src_tf(const TimeArgs &ta, long long b) {
+    const double t = src_time(ta, b);
+    return ta.gk == 0 ? exp(-t) : fma(2.0 * M_PI, cospi(2.0 * t), ta.gc * sinpi(2.0 * t));
 }
 
 // Copy `len` doubles of a global table into chunk-padded shared memory (whole CTA).

@@ -636,7 +636,7 @@ __device__ __forceinline__ DDCols dd_load_tile(const DDStageArgs &a, double *T, 
     const int me = a.stage, other = 1 - a.stage;
     const double *rn_ot = a.rhon + other * n, *rf_ot = a.rhof + other * (n + 1);
     double ampt = 0.0;
-    if (SRC) ampt = a.src_amp * exp(-src_time(a.ta, b));
+    if (SRC) ampt = a.src_amp * src_tf(a.ta, b);
     // every global load of a row is issued before the first use (several rows' worth in flight)
     constexpr int NCW = (DD_WMAX + 31) / 32;  // column slots per lane
     // per-lane column constants, loaded once: the source profile and, for stage 1, which

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(DF_THREADS, 1) df_stage_kernel(DFStageArgs a) 
     const int me = a.stage;
     const long long WW = (long long)W * W;
     double ampt = 0.0;
-    if (SRC) ampt = a.src_amp * exp(-src_time(a.ta, b));
+    if (SRC) ampt = a.src_amp * src_tf(a.ta, b);
     // column constants of thread i (< W): is the column final after stage 0 (rho_other = 0)?
     const int ci = tid;  // owner of column ci for the scalar work (tid < W)
     const bool col = ci < W;

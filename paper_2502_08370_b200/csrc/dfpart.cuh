@@ -368,7 +368,7 @@ __device__ __forceinline__ void dfp_rhs_put(const DFPArgs &x, const DFPTask &t, 
 }
 __device__ __forceinline__ void dfp_ampt(const DFPArgs &x, int grp, double *ampt) {
     for (int s = threadIdx.x; s < DFP_S; s += blockDim.x)
-        ampt[s] = x.src_amp * exp(-src_time(x.ta, (long long)grp * DFP_S + s));
+        ampt[s] = x.src_amp * src_tf(x.ta, (long long)grp * DFP_S + s);
 }
 
 // ------------------------------------------------------------------ forward sweeps ------

@@ -33,7 +33,7 @@ struct IEArgs {
     long long ncols;    // lines of the pass: B n^(dim-1)
     long long inner;    // n^axis: stride along the transformed axis
     int n;
-    // prologue (first forward pass, axis 0): R = U + tau F, F = src_amp e^{-t} prod sin(pi x_d)
+    // prologue (first forward pass, axis 0): R = U + tau F, F = src_amp g(t) prod srcsin(x_d)
     int src, dim;
     double tau, src_amp;
     const double *sinpi;
@@ -56,8 +56,9 @@ __global__ void __launch_bounds__(IE_T) ie_axis_kernel(IEArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 2, wn = warp & 3;  // warp tile: rows wm*32 .. +32, cols wn*16 .. +16
     const int n = a.n;
-    const long long c0 = (long long)blockIdx.x * IE_BN;
-    const int i0 = blockIdx.y * IE_BM;
+    // row tiles fastest: the CTAs that share a block of lines (and read it) run together (L2)
+    const long long c0 = (long long)blockIdx.y * IE_BN;
+    const int i0 = blockIdx.x * IE_BM;
     const bool unit = a.inner == 1;
 
     // this thread's four loads of each B tile: fixed lines, k rows advancing with the k-step
@@ -75,9 +76,9 @@ __global__ void __launch_bounds__(IE_T) ie_axis_kernel(IEArgs a) {
         if (c < a.ncols) {
             const long long o = c / a.inner, q = c - o * a.inner;
             bbase[r] = o * n * a.inner + q;
-            if (PRO && a.src) {  // axis 0: line c = (state b, y [, z]); F = amp e^{-t} sy [sz] sin(pi x)
+            if (PRO && a.src) {  // axis 0: line c = (state b, y [, z]); F = amp g(t) sy [sz] sx
                 const long long per = a.vol / n, b = c / per, yz = c - b * per;
-                double f = a.tau * a.src_amp * exp(-src_time(a.ta, b)) * __ldg(a.sinpi + yz % n);
+                double f = a.tau * a.src_amp * src_tf(a.ta, b) * __ldg(a.sinpi + yz % n);
                 if (a.dim == 3) f *= __ldg(a.sinpi + yz / n);
                 bsrc[r] = f;
             }

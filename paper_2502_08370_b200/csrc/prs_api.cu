@@ -156,6 +156,10 @@ struct prs_ctx {
     double *delta = nullptr;  // = fa or fb after a fine sweep
     double *u0 = nullptr;
     double *sinpi = nullptr, *s2n = nullptr, *s2f = nullptr;
+    // source (R29): F = src_amp g(t) prod_d srcsin[i_d]; kind 1: dim pi^2 + c - 1, e^{-t},
+    // sin(pi x); kind 2: 1, 2 pi cos 2 pi t + (8 pi^2 + c) sin 2 pi t, sin(2 pi x)
+    double src_amp = 0.0;
+    const double *srcsin = nullptr;
     TauFactors fac[3];  // 0 coarse, 1 fine, 2 custom (prs_step)
     DDData dd;
     unsigned long long *red = nullptr;  // [0] update bits, [1] flag, [2] scratch
@@ -378,8 +382,8 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.creact = ctx->creact;
-    a.src_amp = (double)dim * M_PI * M_PI + ctx->p.c - 1.0;
-    a.sinpi = ctx->sinpi;
+    a.src_amp = ctx->src_amp;
+    a.sinpi = ctx->srcsin;
     a.ta = ta;
     a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
     a.invd = f.invdx;
@@ -387,7 +391,7 @@ static int launch_xpass3(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.s2f = ctx->s2f;
     const int dr = (scheme == PRS_DR) ? 1 : 0;
     const int coef = ctx->p.coef_kind;
-    const int src = ctx->p.source_kind;
+    const int src = ctx->p.source_kind != 0;
     const size_t shm = xpass3_smem_bytes(coef);
     void (*kern)(X3Args) = nullptr;
 #define XK(C, D, S_) if (coef == C && dr == D && src == S_) kern = xpass3_kernel<C, D, S_>;
@@ -466,14 +470,14 @@ static int launch_xpass7(prs_ctx *ctx, int scheme, const TauFactors &f, const do
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.creact = ctx->creact;
-    a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
-    a.sinpi = ctx->sinpi;
+    a.src_amp = ctx->src_amp;
+    a.sinpi = ctx->srcsin;
     a.ta = ta;
     a.tab = CoefTab{f.tab, f.tab ? f.tab + X7N : nullptr, f.tab ? f.tab + 2 * X7N : nullptr};
     a.invd = f.invdx;
     a.s2n = ctx->s2n;
     a.s2f = ctx->s2f;
-    const int dr = (scheme == PRS_DR) ? 1 : 0, coef = ctx->p.coef_kind, src = ctx->p.source_kind;
+    const int dr = (scheme == PRS_DR) ? 1 : 0, coef = ctx->p.coef_kind, src = ctx->p.source_kind != 0;
     const int tma = ctx->x7_tma ? 1 : 0;
     if (tma) {
         TRY(get_tmap(ctx, in, B * ctx->vol / LCH, &a.tm_in));
@@ -527,8 +531,8 @@ static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const dou
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.creact = ctx->creact;
-    a.src_amp = (double)dim * M_PI * M_PI + ctx->p.c - 1.0;
-    a.sinpi = ctx->sinpi;
+    a.src_amp = ctx->src_amp;
+    a.sinpi = ctx->srcsin;
     a.ta = ta;
     a.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
     a.invd = f.invdx;
@@ -539,7 +543,7 @@ static int launch_xpass(prs_ctx *ctx, int scheme, const TauFactors &f, const dou
     const int threads = lpb * a.P;
     const int dr = (scheme == PRS_DR) ? 1 : 0;
     const int coef = ctx->p.coef_kind;
-    const int src = ctx->p.source_kind;
+    const int src = ctx->p.source_kind != 0;
     const size_t shm = sizeof(double) * xpass_smem_doubles(lpb, a.S, a.St, coef, threads);
     const long long blocks = (a.nlines + lpb - 1) / lpb;
     void (*kern)(XArgs) = nullptr;
@@ -814,7 +818,10 @@ static int launch_lpass(prs_ctx *ctx, int axis, const TauFactors &f, const doubl
 static int ie_step(prs_ctx *ctx, double tau, const double *in, double *out, long long B, const TimeArgs &ta,
                    const EpiArgs &ep, bool prof);
 static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double *in, double *out,
-                    long long B, const TimeArgs &ta, const EpiArgs &ep, bool prof, long long stride) {
+                    long long B, const TimeArgs &ta_in, const EpiArgs &ep, bool prof, long long stride) {
+    TimeArgs ta = ta_in;
+    ta.gk = ctx->p.source_kind == 2 ? 1 : 0;
+    ta.gc = 8.0 * M_PI * M_PI + ctx->p.c;
     if (scheme == PRS_IE) {
         if (stride != ctx->vol) {
             ctx->err = "internal: padded slice stride on the IE path";
@@ -825,7 +832,7 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
     if (ctx->p.split == 1)
         return dd_step(ctx->dd, scheme, (int)(&f - ctx->fac), in, out, B, ta, ep.kind, ep.gc, ep.gcache,
                        ep.delta, ep.traj, ctx->red, ctx->stream, prof ? ctx : nullptr, ctx->err, ctx->launches,
-                       2.0 * M_PI * M_PI + ctx->p.c - 1.0, ctx->p.source_kind);
+                       ctx->src_amp, ctx->p.source_kind != 0);
     if (stride != ctx->vol) {
         ctx->err = "internal: padded slice stride on a path without stride support";
         return PRS_EUNSUPPORTED;
@@ -838,8 +845,8 @@ static int run_step(prs_ctx *ctx, int scheme, const TauFactors &f, const double 
         x.vol = ctx->vol;
         x.nplanes = B * XY_N;
         x.tau = f.tau;
-        x.src_amp = 3.0 * M_PI * M_PI + ctx->p.c - 1.0;
-        x.sinpi = ctx->sinpi;
+        x.src_amp = ctx->src_amp;
+        x.sinpi = ctx->srcsin;
         x.ta = ta;
         x.tab = CoefTab{f.tab, f.tab + XY_N, f.tab + 2 * XY_N};
         x.offd = -f.tau * ctx->h2inv;  // as setup_const_tab forms it
@@ -896,10 +903,10 @@ static int ie_step(prs_ctx *ctx, double tau, const double *in, double *out, long
     a.ncols = B * (ctx->vol / n);
     a.n = n;
     a.dim = dim;
-    a.src = ctx->p.source_kind;
+    a.src = ctx->p.source_kind != 0;
     a.tau = tau;
-    a.src_amp = (double)dim * M_PI * M_PI + ctx->p.c - 1.0;
-    a.sinpi = ctx->sinpi;
+    a.src_amp = ctx->src_amp;
+    a.sinpi = ctx->srcsin;
     a.ta = ta;
     a.creact = ctx->p.c;
     a.norm = std::pow(2.0 / (double)(n + 1), dim);
@@ -908,7 +915,12 @@ static int ie_step(prs_ctx *ctx, double tau, const double *in, double *out, long
     a.e_delta = ep.delta;
     a.e_traj = ep.traj;
     a.e_red = ctx->red;
-    const dim3 grid((unsigned)((a.ncols + IE_BN - 1) / IE_BN), (unsigned)((n + IE_BM - 1) / IE_BM));
+    const long long gy = (a.ncols + IE_BN - 1) / IE_BN;
+    if (gy > 65535) {
+        ctx->err = "IE step: more than 65535 x 64 lines per batch";
+        return PRS_EUNSUPPORTED;
+    }
+    const dim3 grid((unsigned)((n + IE_BM - 1) / IE_BM), (unsigned)gy);
     double *w[2] = {ctx->ie_w1, ctx->ie_w2};
     const double *src = in;
     if (prof) TRY(prof_begin(ctx));
@@ -1000,7 +1012,12 @@ static int validate(const prs_problem *p, std::string &err) {
         return PRS_EUNSUPPORTED;
     }
     if (p->coef_kind < 0 || p->coef_kind > 2) { err = "coef_kind must be 0, 1 or 2"; return PRS_EINVAL; }
-    if (p->source_kind != 0 && p->source_kind != 1) { err = "source_kind must be 0 or 1"; return PRS_EINVAL; }
+    if (p->source_kind < 0 || p->source_kind > 2) { err = "source_kind must be 0, 1 or 2"; return PRS_EINVAL; }
+    if (p->source_kind == 2 && (p->dim != 2 || p->coef_kind != 0)) {
+        err = "source_kind 2 (the section-5.1 solution sin(2 pi t) sin(2 pi x) sin(2 pi y), PAPER.md:444-449) "
+              "is defined for the 2-D problem with D = I (coef_kind 0)";
+        return PRS_EINVAL;
+    }
     if (p->split != 0 && p->split != 1) { err = "split must be 0 or 1"; return PRS_EINVAL; }
     if (p->split == 1) {
         if (p->dim != 2) { err = "DD splitting is 2-D"; return PRS_EUNSUPPORTED; }
@@ -1098,6 +1115,8 @@ static int create_impl(const prs_problem *prob, int rank, int nranks, Transport 
     ctx->red = ctx->red_base;
     setup_sines<<<(n + 1 + 255) / 256, 256, 0, ctx->stream>>>(n, ctx->h, ctx->sinpi, ctx->s2n, ctx->s2f);
     ctx->launches++;
+    ctx->src_amp = prob->source_kind == 2 ? 1.0 : (double)prob->dim * M_PI * M_PI + prob->c - 1.0;
+    ctx->srcsin = prob->source_kind == 2 ? ctx->s2n : ctx->sinpi;
     CKC(cudaGetLastError());
     if (prob->split == 1) {
         int drc = dd_init(ctx->dd, *prob, ctx->h, ctx->h2inv, ctx->stream, ctx->err);
@@ -1107,7 +1126,7 @@ static int create_impl(const prs_problem *prob, int rank, int nranks, Transport 
             *out = nullptr;
             return drc;
         }
-        ctx->dd.sinpi = ctx->sinpi;
+        ctx->dd.sinpi = ctx->srcsin;
     }
     if (prob->G == PRS_IE || prob->F == PRS_IE) {
         CKC(cudaMalloc(&ctx->ie_S, sizeof(double) * (size_t)n * n));
@@ -1367,7 +1386,7 @@ static int local_start(const prs_ctx *ctx) {
 static bool sweep2_ok(const prs_ctx *ctx) {
     const int n = ctx->p.n;
     return !ctx->no_sweep2 && ctx->p.dim == 2 && ctx->p.split == 0 && ctx->p.coef_kind == 0 &&
-           ctx->p.G != PRS_IE && ctx->p.F != PRS_IE &&
+           ctx->p.G != PRS_IE && ctx->p.F != PRS_IE && ctx->p.source_kind != 2 &&
            (n == 32 || n == 64 || n == 128 || n == 256);
 }
 
@@ -1384,13 +1403,13 @@ static int launch_sweep2(prs_ctx *ctx, const double *in, double *out, const doub
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.creact = ctx->creact;
-    a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
-    a.sinpi = ctx->sinpi;
+    a.src_amp = ctx->src_amp;
+    a.sinpi = ctx->srcsin;
     a.slice0 = slice0;
     a.sstride = slice_stride(ctx);
     a.dt = ctx->dt;
     a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
-    const int dr = (ctx->p.F == PRS_DR) ? 1 : 0, src = ctx->p.source_kind, epi = gc ? EPI_DELTA : EPI_STORE;
+    const int dr = (ctx->p.F == PRS_DR) ? 1 : 0, src = ctx->p.source_kind != 0, epi = gc ? EPI_DELTA : EPI_STORE;
     void (*k)(SWArgs) = nullptr;
     size_t shm = 0;
 #define SK(N_, D, S_, E)                                                   \
@@ -1445,13 +1464,13 @@ static int launch_chain2x(prs_ctx *ctx, double *traj, double *gcache, const doub
     a.tau = f.tau;
     a.h2inv = ctx->h2inv;
     a.creact = ctx->creact;
-    a.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
-    a.sinpi = ctx->sinpi;
+    a.src_amp = ctx->src_amp;
+    a.sinpi = ctx->srcsin;
     a.slice0 = slice0 >= 0 ? slice0 : ctx->first + i0;
     a.sstride = 1;
     a.dt = ctx->dT;
     a.tab = CoefTab{f.tab, f.tab + n, f.tab + 2 * n};
-    const int dr = (ctx->p.G == PRS_DR) ? 1 : 0, src = ctx->p.source_kind;
+    const int dr = (ctx->p.G == PRS_DR) ? 1 : 0, src = ctx->p.source_kind != 0;
     void (*k)(SWArgs) = nullptr;
     size_t shm = 0;
 #define SK(N_, D, S_, E)                                                   \
@@ -1640,14 +1659,14 @@ static int gp_phase1(prs_ctx *ctx, int b, const double *in, double *v, int slice
     x.tau = f.tau;
     x.h2inv = ctx->h2inv;
     x.creact = ctx->creact;
-    x.src_amp = 2.0 * M_PI * M_PI + ctx->p.c - 1.0;
-    x.sinpi = ctx->sinpi;
+    x.src_amp = ctx->src_amp;
+    x.sinpi = ctx->srcsin;
     x.ta = coarse_time(ctx, slice);
     x.tab = CoefTab{f.tab, f.tab ? f.tab + n : nullptr, f.tab ? f.tab + 2 * n : nullptr};
     x.invd = f.invdx;
     x.s2n = ctx->s2n;
     x.s2f = ctx->s2f;
-    const int coef = ctx->p.coef_kind, src = ctx->p.source_kind;
+    const int coef = ctx->p.coef_kind, src = ctx->p.source_kind != 0;
     void (*kx)(X3Args) = nullptr;
 #define XK(C, S_) if (coef == C && src == S_) kx = xpass3_kernel<C, 0, S_>;
     XK(0, 0) XK(0, 1) XK(1, 0) XK(1, 1)
@@ -2143,6 +2162,8 @@ int prs_step(prs_ctx *ctx, int scheme, double tau, double t_next, const double *
         ta.tmul = 0;
         ta.toff = 1;
         ta.tstep = t_next;
+        ta.gk = ctx->p.source_kind == 2 ? 1 : 0;
+        ta.gc = 8.0 * M_PI * M_PI + ctx->p.c;
         EpiArgs ep;
         TRY(ie_step(ctx, tau, in, out, 1, ta, ep, false));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -2232,6 +2253,10 @@ int prs_set_coarse_mode(prs_ctx *ctx, int mode, int bands) {
     const bool pow2 = P >= 1 && (P & (P - 1)) == 0 && (n & (n - 1)) == 0;
     if (ctx->cyclic) {
         ctx->err = "space-parallel G: contiguous slice ownership only";
+        return PRS_EUNSUPPORTED;
+    }
+    if (ctx->p.source_kind == 2) {
+        ctx->err = "space-parallel G: source_kind 0 or 1";
         return PRS_EUNSUPPORTED;
     }
     if (ctx->p.dim != 2 || ctx->p.split != 0 || ctx->p.G != PRS_FIE || !pow2 || n > 4096 || n % (L5RB * P) != 0 ||

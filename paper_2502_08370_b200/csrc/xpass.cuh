@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) xpass_kernel(XArgs a) {
     // ---- load + fused stage-1 right-hand side ----
     double ampt = 0.0, sj = 0.0;
     if (SRC && active) {
-        ampt = a.src_amp * exp(-src_time(a.ta, b));
+        ampt = a.src_amp * src_tf(a.ta, b);
         sj = (a.dim == 2) ? a.sinpi[j] : a.sinpi[j % n] * a.sinpi[j / n];
     }
     const bool has_m = j > 0, has_p = j < n - 1;

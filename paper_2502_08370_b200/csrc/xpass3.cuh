@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(X3T, 1) xpass3_kernel(const __grid_constant__ 
         }
         if (COEF) s.hsx = __ldg(a.s2n + ((a.dim == 2) ? jj : jj % n));
         if (SRC) {
-            const double ampt = a.src_amp * exp(-src_time(a.ta, bs));
+            const double ampt = a.src_amp * src_tf(a.ta, bs);
             const double sj =
                 (a.dim == 2) ? __ldg(a.sinpi + jj) : __ldg(a.sinpi + jj % n) * __ldg(a.sinpi + jj / n);
             s.srcf = a.tau * ampt * sj;

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(X7T, 2) xpass7_kernel(const __grid_constant__ 
             // the pivot before this CTA's first point (the partner's last one) for chunk 0
             if (crank == 1 && k == 0) s.idm1 = __ldg(a.invd + (long long)jj * n + hoff - 1);
         }
-        if (SRC) s.srcf = a.tau * a.src_amp * exp(-src_time(a.ta, gg >> 12)) * __ldg(a.sinpi + jj);
+        if (SRC) s.srcf = a.tau * a.src_amp * src_tf(a.ta, gg >> 12) * __ldg(a.sinpi + jj);
         return s;
     };
 

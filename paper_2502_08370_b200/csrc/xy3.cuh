@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(XY_T, 2) xy3_kernel(XYArgs a) {
             ty[2 * XY_S + cpad(e)] = __ldg(a.tab.cc + e);
         }
         double sz = 0.0;
-        if (SRC) sz = a.tau * a.src_amp * exp(-src_time(a.ta, b)) * __ldg(a.sinpi + z);
+        if (SRC) sz = a.tau * a.src_amp * src_tf(a.ta, b) * __ldg(a.sinpi + z);
 #pragma unroll
         for (int k = 0; k < NLD; ++k) {
             const int e = tid + k * XY_T, r = e >> 6, x2 = (e & 63) * 2;

@@ -32,13 +32,14 @@ class Problem:
     dd_strips: int = 8
     dd_overlap: int = 8
     dd_ramp: int = 0       # 0 linear, 1 cosine
-    source: int = 0        # 0 none, 1 manufactured (u = e^{-t} prod sin(pi x_d))
+    source: int = 0        # 0 none, 1 manufactured (u = e^{-t} prod sin(pi x_d)),
+                           # 2 the section-5.1 solution u = sin(2 pi t) sin(2 pi x) sin(2 pi y) (2-D, D = I)
     T: float = 1.0
     N: int = 8
     s: int = 16
     G: int = FIE
     F: int = FIE
-    init: str = "phi"      # "phi" | "modes"
+    init: str = "phi"      # "phi" | "modes" | "random" | "zero"
     seed: int = 0
     kmax: int = 0          # 0 -> N (finite termination)
     tol: float = 1e-10
@@ -79,11 +80,10 @@ CONFIGS = {
     # (d11 = d22 = 1/(2 + cos 3pi x cos 2pi y), d12 = 1/4), the paper's Parareal/FIE-FIE
     "c5": Problem(dim=2, n=1024, c=1.0, coef=2, split=1, dd_strips=8, dd_overlap=8, dd_ramp=0,
                   source=1, N=32, s=64, G=FIE, F=FIE, init="phi"),
-    # c6: the Parareal/IE-IE baseline on the grid of the paper's
-    # section-5.1 experiments: h = 1e-3 (n = 999), T = 1, Delta T = 0.05
-    # (N = 20), delta t = 2.5e-3 (s = 20), D = I, c = 0; the manufactured e^{-t} sin sin source
-    # stands in for the paper's sin(2 pi t) sin(2 pi x) sin(2 pi y) solution (R29)
-    "c6": Problem(dim=2, n=999, c=0.0, source=1, N=20, s=20, G=IE, F=IE, init="phi"),
+    # c6: the Parareal/IE-IE baseline on the paper's section-5.1 problem
+    # (PAPER.md:444-453): u = sin(2 pi t) sin(2 pi x) sin(2 pi y), D = I, c = 0 (R29),
+    # h = 1e-3 (n = 999), T = 1, Delta T = 0.05 (N = 20), delta t = 2.5e-3 (s = 20), u(0) = 0
+    "c6": Problem(dim=2, n=999, c=0.0, source=2, N=20, s=20, G=IE, F=IE, init="zero"),
 }
 
 
@@ -145,6 +145,8 @@ def initial_state(prob: Problem) -> np.ndarray:
             # u[y][x]: y index l-mode, x index j-mode
             u += a * np.outer(_sines(n, l), _sines(n, j))
         return u
+    if prob.init == "zero":  # u(0) = sin(0) sin sin = 0 of the section-5.1 solution
+        return np.zeros((n,) * prob.dim)
     if prob.init == "random":
         rng = np.random.default_rng(prob.seed)
         return rng.standard_normal((n,) * prob.dim)

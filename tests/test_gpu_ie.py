@@ -141,3 +141,48 @@ def test_ie_step_needs_ie_context():
         ctx.step(IE, 0.1, 0.1, x, torch.empty_like(x))
     assert ei.value.code == prs.PRS_EINVAL
     ctx.close()
+
+
+# ------------------------------ the section-5.1 problem: source_kind 2 on every kernel path
+S51_PARAREAL_CASES = [
+    Problem(dim=2, n=40, c=0.0, source=2, N=5, s=4, G=IE, F=IE, init="zero"),
+    Problem(dim=2, n=64, c=0.0, source=2, N=4, s=4, G=FIE, F=DR, init="zero"),    # per-step kernels
+    Problem(dim=2, n=48, c=1.0, source=2, N=4, s=3, G=DR, F=DR, init="random"),
+    Problem(dim=2, n=32, c=0.0, split=1, dd_strips=4, dd_overlap=2, source=2, N=4, s=3, G=FIE, F=FIE,
+            init="zero"),
+    Problem(dim=2, n=32, c=0.0, split=1, dd_strips=2, dd_overlap=4, source=2, N=4, s=3, G=IE, F=DR,
+            init="zero"),
+]
+
+
+@pytest.mark.parametrize("p", S51_PARAREAL_CASES, ids=lambda p: p.label())
+def test_section51_parareal_iterates_match_oracle(p):
+    from tests.test_gpu_parity import _parareal_vs_oracle
+    _parareal_vs_oracle(p)
+
+
+@pytest.mark.parametrize("n", [100, 1024, 2048, 4096])
+def test_section51_single_steps_long_lines(n):
+    """FIE and DR steps with the section-5.1 source through the long-line kernels (xpass3 / xpass7
+    + lpass) at the benchmarked line lengths, against the oracle"""
+    prs = prs_mod()
+    p = Problem(dim=2, n=n, c=0.0, source=2, N=4, s=3, G=FIE, F=DR)
+    o = oracle.Oracle(p)
+    ctx = prs.Context(p)
+    # smooth data (the literal vs algebraic DR forms differ by eps tau ||A U||, DESIGN.md R13)
+    x = np.arange(1, n + 1) / (n + 1)
+    u = 0.1 * np.outer(np.sin(3 * np.pi * x), np.sin(2 * np.pi * x))
+    for scheme, tau, t1 in ((FIE, 1e-3, 0.3), (DR, 1e-4, 0.77)):
+        want = o.step(scheme, tau, t1, u)
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        ctx.step(scheme, tau, t1, dev(u), out)
+        assert nerr(host(out), want, u, want) <= TOL, scheme
+    ctx.close()
+
+
+def test_section51_source_rejected_outside_2d_constant_d():
+    prs = prs_mod()
+    for p in (Problem(dim=3, n=8, source=2, N=2, s=2), Problem(dim=2, n=16, coef=1, source=2, N=2, s=2)):
+        with pytest.raises(prs.PrsError) as ei:
+            prs.Context(p)
+        assert ei.value.code == prs.PRS_EINVAL

@@ -294,7 +294,8 @@ def _parareal_vs_oracle(p, finite_termination=True):
         e = float(np.max(np.abs(gtrajs[k] - ctrajs[k]))) / scale
         assert e <= TOL, (k, e)
     for k in range(K):
-        scale = max(1.0, max(float(np.max(np.abs(t))) for t in ctrajs[: k + 2]) / np.max(np.abs(u0)))
+        u0n = float(np.max(np.abs(u0))) or 1.0  # the update is normalised by ||U_0|| (1 for U_0 = 0)
+        scale = max(1.0, max(float(np.max(np.abs(t))) for t in ctrajs[: k + 2]) / u0n)
         assert abs(gupds[k] - cupds[k]) <= TOL * scale, (k, gupds[k], cupds[k])
     if not finite_termination:
         return
