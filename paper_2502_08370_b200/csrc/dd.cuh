@@ -1791,6 +1791,25 @@ inline int dd_init(DDData &d, const prs_problem &p, double h, double h2inv, cuda
 }
 
 // full tensor: block-Thomas factors of every block of both colours (one CTA per block)
+// Rows per partition of the partitioned full-tensor sweeps: DFP_M, shortened (not below 48) when
+// that lets two state groups of a colour's blocks fill the SMs in one wave -- c5: 4 blocks x 2
+// groups x 16 partitions of 64 rows = 128 CTAs on 148 SMs becomes 18 partitions of 57 = 144.
+inline int dfp_rows(const DDData &d) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    const int nbmax = (int)std::max(d.bi0[0].size(), d.bi0[1].size());
+    const int P0 = (d.n + DFP_M - 1) / DFP_M, P1 = nbmax > 0 ? sms / (2 * nbmax) : 0;
+    if (P1 > P0) {
+        const int M = (d.n + P1 - 1) / P1;
+        if (M >= 48) return M;
+    }
+    return DFP_M;
+}
+
 inline int df_factors(DDData &d, int slot, double tau, cudaStream_t st, std::string &err) {
     for (int col = 0; col < 2; ++col) {
         const size_t nb = d.bi0[col].size();
@@ -1826,7 +1845,7 @@ inline int df_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
                                                                dP);
         if (d.dfpart) {
             // the partition products A_p^T, Pp_p^T: the sweeps of dfpart.cuh on unit columns
-            const int P = (d.n + DFP_M - 1) / DFP_M;
+            const int Mr = dfp_rows(d), P = (d.n + Mr - 1) / Mr;
             std::vector<double *> hA(nb), hPp(nb);
             for (size_t k = 0; k < nb; ++k) {
                 const size_t bytes = sizeof(double) * (size_t)P * d.bW[col][k] * d.bW[col][k];
@@ -1852,6 +1871,7 @@ inline int df_factors(DDData &d, int slot, double tau, cudaStream_t st, std::str
             x.nblk = (int)nb;
             x.ngrp = (DF_WMAX + DFP_S - 1) / DFP_S;  // unit columns in groups of DFP_S
             x.P = P;
+            x.M = Mr;
             x.bi0 = d.d_bi0[col];
             x.bW = d.d_bW[col];
             x.ET = dE;
@@ -2046,7 +2066,7 @@ inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, doubl
     const int n = d.n;
     if (Btot < 0) Btot = B;
     if (d.full && d.dfpart) {
-        const int P = (n + DFP_M - 1) / DFP_M, ngrp = (int)((B + DFP_S - 1) / DFP_S);
+        const int Mr = dfp_rows(d), P = (n + Mr - 1) / Mr, ngrp = (int)((B + DFP_S - 1) / DFP_S);
         const int nbmax = (int)std::max(d.bi0[0].size(), d.bi0[1].size());
         const long long bgs = (long long)nbmax * ngrp;
         if (bgs > d.dcap) {
@@ -2078,6 +2098,7 @@ inline int dd_step_impl(DDData &d, int scheme, int slot, const double *in, doubl
             x.nblk = (int)d.bi0[stage].size();
             x.ngrp = ngrp;
             x.P = P;
+            x.M = Mr;
             x.bi0 = d.d_bi0[stage];
             x.bW = d.d_bW[stage];
             x.ET = d.d_ET[slot][stage];

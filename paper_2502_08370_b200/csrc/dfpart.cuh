@@ -28,7 +28,7 @@
 
 namespace prs {
 
-constexpr int DFP_M = 64;             // rows per partition
+constexpr int DFP_M = 64;             // rows per partition (default; dfp_rows in dd.cuh)
 constexpr int DFP_S = 16;             // right-hand sides per CTA (two n-tiles of 8)
 constexpr int DFP_SP = DFP_S + 4;     // shared row stride of a W x S tile (conflict-free fragments)
 constexpr int DFP_NW = DF_WMAX / 16;  // 9 warps: m-tiles w and w + 9 of the W <= 144 rows
@@ -42,6 +42,7 @@ struct DFPArgs {
     double *V;
     long long vol;
     int n, B, stage, nblk, ngrp, P;  // P = partitions per block, ngrp = state groups (of DFP_S)
+    int M;                           // rows per partition (dfp_rows: DFP_M, shortened to fill the SMs)
     const int *bi0, *bW;
     const double *const *ET, *const *PI;   // per block: E_l^T and P_l^{-1} (n W^2 each)
     const double *const *AT, *const *PpT;  // per block: A_p^T and Pp_p^T (P W^2 each)
@@ -268,8 +269,8 @@ struct DFPTask {
         blk = (int)(bg / x.ngrp);
         W = x.bW[blk];
         i0 = x.bi0[blk];
-        a = p * DFP_M;
-        m = min(DFP_M, x.n - a);
+        a = p * x.M;
+        m = min(x.M, x.n - a);
         PRS_CHECK(blk < x.nblk && W <= DF_WMAX && m > 0 && i0 >= 0 && i0 + W <= x.n, "full-tensor task");
     }
 };
